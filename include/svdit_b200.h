@@ -1,0 +1,174 @@
+/*
+ * svdit_b200.h — C ABI of the B200-native Sparse-vDiT attention hot path.
+ *
+ * This is the drop-in boundary for the reference's operator layer
+ * (svdit 0.1.0, /root/reference/pkg/src/svdit).  The reference has no FFI:
+ * it is pure NumPy.  Each entry point below replaces one Python function of
+ * the reference's hot path; the Python shim in paper_2506_03065_b200/ binds
+ * them with ctypes and keeps the reference signatures.
+ *
+ *   reference (file:line)                              replaced by
+ *   layout.py:135-158  block_grid(layout)              svd_grid_size / svd_grid_arrays
+ *   patterns.py:334-339 frame_period(grid)             svd_frame_period
+ *   patterns.py:377-417 build_mask(spec, grid)         svd_mask_build
+ *   attention.py:164-183 group_heads(assignment, grid) svd_plan_create + svd_plan_group_* accessors
+ *   attention.py:186-212 fused_layer_attention(...)    svd_attn_fwd
+ *   attention.py:57-98  sparse_attention(q,k,v,mask)   svd_plan_create_from_masks + svd_attn_fwd
+ *   attention.py:101-105 full_mask_attention(...)      svd_plan_create (FULL spec) + svd_attn_fwd
+ *   attention.py:51-54  skip_attention(...)            svd_plan_create (SKIP spec) + svd_attn_fwd
+ *
+ * Conventions
+ *  - Every function returns an svd_status; on failure a message is available
+ *    from svd_last_error() (thread-local).  Status codes map 1:1 onto the
+ *    reference's exception classes (errors.py:9-34).
+ *  - Plans are immutable once created and may be shared across threads and
+ *    CUDA streams.  Device-side plan tables are uploaded lazily, once per
+ *    device, on the first svd_attn_fwd call on that device.
+ *  - Q/K/V/O are caller-owned device buffers of bf16, addressed through
+ *    element strides for the logical [B, H, N, d] view, so both [B,H,N,d]
+ *    and [B,N,H,d] storage work without copies.
+ *  - svd_attn_fwd is stream-ordered and never synchronises the host.
+ */
+#ifndef SVDIT_B200_H
+#define SVDIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum svd_status {
+  SVD_OK = 0,
+  SVD_ERR_SHAPE = 1,            /* errors.py:13  ShapeError          */
+  SVD_ERR_DEGENERATE_ROW = 2,   /* errors.py:17  DegenerateRowError  */
+  SVD_ERR_DEGENERATE_MASK = 3,  /* errors.py:21  DegenerateMaskError */
+  SVD_ERR_CONFIG = 4,           /* errors.py:25  ConfigError         */
+  SVD_ERR_CUDA = 5,             /* CUDA runtime / driver failure      */
+  SVD_ERR_UNSUPPORTED = 6,      /* shape outside the kernel's support */
+  SVD_ERR_INTERNAL = 7
+} svd_status;
+
+typedef enum svd_mode {         /* patterns.py:189-194 Mode */
+  SVD_FULL = 0,
+  SVD_SKIP = 1,
+  SVD_DIAGONAL = 2,
+  SVD_MULTI_DIAGONAL = 3,
+  SVD_VERTICAL_STRIPE = 4
+} svd_mode;
+
+/* layout.py:26-31 TokenLayout */
+typedef struct svd_layout {
+  int64_t text_tokens;
+  int64_t frames;
+  int64_t tokens_per_frame;
+  int64_t block_size;
+} svd_layout;
+
+/* patterns.py:208-233 PatternSpec.  period <= 0 encodes None (frame period);
+ * n_stripes < 0 encodes stripes=None (unresolved).  Stripes may be given in
+ * any order with duplicates: they are normalised to sorted-unique exactly as
+ * PatternSpec.__post_init__ does (patterns.py:232-233). */
+typedef struct svd_spec {
+  int32_t mode;
+  int32_t halfwidth;
+  int32_t period;
+  int32_t md_halfwidth;
+  int32_t stripe_count;
+  int32_t include_diagonal;
+  int32_t n_stripes;
+  const int64_t* stripes;
+} svd_spec;
+
+typedef struct svd_plan svd_plan;
+
+typedef struct svd_plan_info {
+  int64_t n_tokens;            /* N                                            */
+  int64_t n_blocks;            /* nb = ceil(N / block_size)                    */
+  int64_t n_segments;          /* ceil(N / 64): the kernel's 64-token grain    */
+  int32_t n_heads;
+  int32_t n_groups;
+  int32_t fine_mask;           /* 1 when block_size is not a multiple of 64    */
+  int32_t sharded;             /* 1 for a svd_plan_shard() view                */
+  int64_t n_work_items;        /* CTAs per batch entry                         */
+  int64_t n_kv_entries;        /* 128-key tiles over all distinct KV lists     */
+  int64_t computed_tiles;      /* 128x128 MMA tiles issued per batch entry     */
+  double  active_pairs;        /* sum over heads, active (qb,kb): |qb|*|kb|;   */
+                               /* active FLOPs = 4 * d * active_pairs          */
+                               /* (costmodel.py:26-32 convention)              */
+  double  dense_pairs;         /* N^2 * H                                      */
+} svd_plan_info;
+
+/* Thread-local text of the last error (never NULL). */
+const char* svd_last_error(void);
+/* Library build string (arch, version). */
+const char* svd_version(void);
+
+/* ---- layout.py:135-158 block_grid ------------------------------------- */
+int svd_grid_size(const svd_layout* layout, int64_t* n_tokens, int64_t* n_blocks);
+/* bounds: nb+1 entries; has_text, mixed: nb bytes; frame_index: nb entries. */
+int svd_grid_arrays(const svd_layout* layout, int64_t* bounds, uint8_t* has_text,
+                    uint8_t* mixed, int64_t* frame_index);
+/* patterns.py:334-339 frame_period (round-half-even, clamped to >= 1). */
+int svd_frame_period(const svd_layout* layout, int64_t* period);
+
+/* ---- patterns.py:377-417 build_mask ------------------------------------ */
+/* active: nb*nb bytes (row-major, 1 = active).  For SKIP *is_skip = 1 and
+ * active is left untouched (the reference returns active=None). */
+int svd_mask_build(const svd_layout* layout, const svd_spec* spec, uint8_t* active,
+                   int32_t* is_skip);
+
+/* ---- attention.py:164-183 group_heads + the kernel schedule ------------ */
+int svd_plan_create(const svd_layout* layout, const svd_spec* specs, int32_t n_heads,
+                    svd_plan** plan);
+/* An explicit-mask plan (sparse_attention on a caller-built BlockMask):
+ * group_skip[g] != 0 marks a SKIP group (mask ignored); masks holds
+ * n_groups*nb*nb bytes; head_group[h] in [0, n_groups). */
+int svd_plan_create_from_masks(const svd_layout* layout, int32_t n_groups,
+                               const int32_t* group_skip, const uint8_t* masks,
+                               const int32_t* head_group, int32_t n_heads, svd_plan** plan);
+void svd_plan_destroy(svd_plan* plan);
+int svd_plan_get_info(const svd_plan* plan, svd_plan_info* info);
+/* Group g of the reference grouping: first-occurrence order, ascending heads. */
+int svd_plan_group_heads(const svd_plan* plan, int32_t g, int32_t* heads, int32_t* n_heads,
+                         int32_t* is_skip);
+/* Block mask of group g (nb*nb bytes); SKIP groups return SVD_ERR_CONFIG. */
+int svd_plan_group_mask(const svd_plan* plan, int32_t g, uint8_t* active);
+/* CSR of group g's active key blocks, ascending per row
+ * (patterns.py:363-366 active_key_blocks).  row_ptr: nb+1; col_idx: nnz. */
+int svd_plan_group_nnz(const svd_plan* plan, int32_t g, int64_t* nnz);
+int svd_plan_group_csr(const svd_plan* plan, int32_t g, int64_t* row_ptr, int64_t* col_idx);
+/* Restrict the plan's work items to one rank's share (LPT by tile cost) for
+ * head/q-range sharding over world ranks.  The shard writes its rows into
+ * a packed [rows, d] buffer; svd_plan_shard_rows() reports the row count and
+ * the (head, token) of every packed row (for the all-gather unpack). */
+int svd_plan_shard(const svd_plan* plan, int32_t world, int32_t rank, svd_plan** shard);
+int svd_plan_shard_rows(const svd_plan* shard, int64_t* n_rows, int32_t* row_head,
+                        int32_t* row_token);
+
+/* Kernel schedule dump (tests / tooling): items as 12 int32 each
+ * {head, group, kv_begin, kv_count, qseg[4], out_base, 0, 0, 0} and KV
+ * entries as 4 int32 each {kseg0, kseg1, flags, 0}. */
+int svd_plan_schedule(const svd_plan* plan, int32_t* items, int32_t* kv);
+
+/* ---- attention.py:186-212 fused_layer_attention (bf16, sm_100a) -------- */
+/* strides: 4 element strides each for the logical [B, H, N, tensor_dim]
+ * view.  head_dim is the true d (softmax scale 1/sqrt(d)); tensor_dim is the
+ * stored width, 64 or 128 (head_dim <= tensor_dim, padded with zeros).
+ * For a shard plan, o is the packed [rows, tensor_dim] buffer, o_strides[2]
+ * its row stride.  dtype: 0 = bf16 (only). */
+int svd_attn_fwd(const svd_plan* plan, const void* q, const void* k, const void* v, void* o,
+                 const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                 const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                 int32_t dtype, void* stream);
+
+/* Scatter a gathered [world * max_rows, d] buffer of packed shard rows back
+ * into O [B=1, H, N, d] (the multi-GPU reassembly after the NCCL all-gather). */
+int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, int64_t n_rows,
+                    const void* packed, int64_t packed_row_stride, void* o,
+                    const int64_t* o_strides, int32_t head_dim, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVDIT_B200_H */

@@ -1,0 +1,414 @@
+"""Attention operators — the reference API of attention.py, executed by the
+native plan (C++) and the sm_100a forward kernel.
+
+Mirrors: _check_qkv (attention.py:27-33), dense_attention (:36-41),
+skip_attention (:51-54), sparse_attention (:57-98), full_mask_attention
+(:101-105), HeadGroup (:149-161), group_heads (:164-183),
+fused_layer_attention (:186-212).
+
+Tensor contract.  Inputs are rank-4 [B, H, N, d].  CUDA torch tensors run
+in place (bf16 is used as is; other float dtypes are cast to bf16) and the
+result is a bf16 CUDA tensor.  NumPy inputs (the reference's own type) are
+moved to the current CUDA device, computed in bf16 and returned as float32
+NumPy arrays.  There is no CPU compute path: without a CUDA device the
+attention operators raise.
+"""
+
+from __future__ import annotations
+
+import weakref
+from collections import OrderedDict
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ConfigError, DegenerateRowError, ShapeError
+from .layout import BlockGrid, TokenLayout
+from .patterns import BlockMask, Mode, PatternSpec, full_spec, skip_spec
+
+# ---------------------------------------------------------------- native plan
+
+
+class LayerPlan:
+    """One layer's head->pattern assignment lowered to the kernel schedule.
+
+    Wraps an immutable native svd_plan: reference-exact grouping and masks
+    plus the work items / KV tile lists the forward kernel consumes.
+    """
+
+    def __init__(self, handle: int, layout: TokenLayout, n_heads: int, sharded: bool = False):
+        self._handle = nat.c_void_p(handle)
+        self.layout = layout
+        self.n_heads = n_heads
+        self.sharded = sharded
+        self._dev_rows = None
+        self._finalizer = weakref.finalize(self, nat.lib().svd_plan_destroy, nat.c_void_p(handle))
+
+    # -- construction
+    @classmethod
+    def from_specs(cls, assignment, layout: TokenLayout) -> "LayerPlan":
+        keep: list = []
+        n = len(assignment)
+        if n < 1:
+            raise ConfigError("assignment must name at least one head")
+        specs = (nat.SvdSpec * n)(*[nat.make_spec(s, keep) for s in assignment])
+        out = nat.c_void_p()
+        nat.check(nat.lib().svd_plan_create(nat.make_layout(layout), specs, n, nat.ctypes.byref(out)))
+        return cls(out.value, layout, n)
+
+    @classmethod
+    def from_masks(cls, layout: TokenLayout, group_masks, head_group) -> "LayerPlan":
+        """group_masks: list of bool [nb, nb] arrays or None (SKIP)."""
+        nb = layout.n_blocks
+        ng = len(group_masks)
+        masks = np.ones((ng, nb, nb), dtype=np.uint8)
+        skip = np.zeros(ng, dtype=np.int32)
+        for g, m in enumerate(group_masks):
+            if m is None:
+                skip[g] = 1
+            else:
+                masks[g] = np.asarray(m, dtype=bool)
+        hg = np.ascontiguousarray(np.asarray(head_group, dtype=np.int32))
+        out = nat.c_void_p()
+        nat.check(nat.lib().svd_plan_create_from_masks(
+            nat.make_layout(layout), ng, nat.ptr(skip), nat.ptr(masks), nat.ptr(hg), int(hg.size),
+            nat.ctypes.byref(out)))
+        return cls(out.value, layout, int(hg.size))
+
+    # -- queries
+    @property
+    def handle(self) -> nat.c_void_p:
+        return self._handle
+
+    @property
+    def info(self) -> nat.SvdPlanInfo:
+        info = nat.SvdPlanInfo()
+        nat.check(nat.lib().svd_plan_get_info(self._handle, nat.ctypes.byref(info)))
+        return info
+
+    def group_heads(self, g: int) -> tuple[tuple[int, ...], bool]:
+        n = nat.c_int32(0)
+        skip = nat.c_int32(0)
+        nat.check(nat.lib().svd_plan_group_heads(self._handle, g, None, nat.ctypes.byref(n),
+                                                 nat.ctypes.byref(skip)))
+        heads = np.empty(n.value, dtype=np.int32)
+        nat.check(nat.lib().svd_plan_group_heads(self._handle, g, nat.ptr(heads),
+                                                 nat.ctypes.byref(n), nat.ctypes.byref(skip)))
+        return tuple(int(h) for h in heads), bool(skip.value)
+
+    def group_mask(self, g: int) -> np.ndarray:
+        nb = self.layout.n_blocks
+        active = np.empty((nb, nb), dtype=np.uint8)
+        nat.check(nat.lib().svd_plan_group_mask(self._handle, g, nat.ptr(active)))
+        return active.view(bool)
+
+    def group_csr(self, g: int) -> tuple[np.ndarray, np.ndarray]:
+        nnz = nat.c_int64(0)
+        nat.check(nat.lib().svd_plan_group_nnz(self._handle, g, nat.ctypes.byref(nnz)))
+        row_ptr = np.empty(self.layout.n_blocks + 1, dtype=np.int64)
+        col_idx = np.empty(max(nnz.value, 1), dtype=np.int64)
+        nat.check(nat.lib().svd_plan_group_csr(self._handle, g, nat.ptr(row_ptr), nat.ptr(col_idx)))
+        return row_ptr, col_idx[: nnz.value]
+
+    def schedule(self) -> tuple[np.ndarray, np.ndarray]:
+        """The kernel schedule: items [n, 12] int32 and KV tiles [m, 4] int32."""
+        info = self.info
+        items = np.zeros((max(info.n_work_items, 1), 12), dtype=np.int32)
+        kv = np.zeros((max(info.n_kv_entries, 1), 4), dtype=np.int32)
+        nat.check(nat.lib().svd_plan_schedule(self._handle, nat.ptr(items), nat.ptr(kv)))
+        return items[: info.n_work_items], kv[: info.n_kv_entries]
+
+    def active_flops(self, head_dim: int) -> float:
+        """costmodel.py:26-32 convention: 4 * d * sum of active (qb, kb) token pairs."""
+        return 4.0 * head_dim * self.info.active_pairs
+
+    def dense_flops(self, head_dim: int) -> float:
+        return 4.0 * head_dim * self.info.dense_pairs
+
+    # -- multi-GPU
+    def shard(self, world: int, rank: int) -> "LayerPlan":
+        out = nat.c_void_p()
+        nat.check(nat.lib().svd_plan_shard(self._handle, world, rank, nat.ctypes.byref(out)))
+        return LayerPlan(out.value, self.layout, self.n_heads, sharded=True)
+
+    def shard_rows(self) -> tuple[np.ndarray, np.ndarray]:
+        n = nat.c_int64(0)
+        nat.check(nat.lib().svd_plan_shard_rows(self._handle, nat.ctypes.byref(n), None, None))
+        heads = np.empty(max(n.value, 1), dtype=np.int32)
+        toks = np.empty(max(n.value, 1), dtype=np.int32)
+        nat.check(nat.lib().svd_plan_shard_rows(self._handle, nat.ctypes.byref(n), nat.ptr(heads),
+                                                nat.ptr(toks)))
+        return heads[: n.value], toks[: n.value]
+
+    # -- execution
+    def forward(self, q, k, v, out, head_dim: int | None = None, stream=None) -> None:
+        """Launch the fused layer kernel on prepared bf16 CUDA tensors.
+
+        q, k, v: [B, H, N, D] views with unit stride on D (D = 64 or 128);
+        out: [B, H, N, D] (or the packed [rows, D] buffer of a shard plan).
+        No host synchronisation; runs on `stream` (default: current stream).
+        """
+        import torch
+
+        d_t = q.shape[-1]
+        hd = int(head_dim if head_dim is not None else d_t)
+        if stream is None:
+            stream = torch.cuda.current_stream(q.device)
+        st = [nat.i64x4(t.stride()) for t in (q, k, v)]
+        if self.sharded:
+            ost = nat.i64x4((0, 0, out.stride(0), out.stride(1)))
+            batch = 1
+        else:
+            ost = nat.i64x4(out.stride())
+            batch = q.shape[0]
+        nat.check(nat.lib().svd_attn_fwd(
+            self._handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
+            nat.c_void_p(v.data_ptr()), nat.c_void_p(out.data_ptr()), st[0], st[1], st[2], ost,
+            int(batch), hd, int(d_t), 0, nat.c_void_p(stream.cuda_stream)))
+
+
+_PLAN_CACHE: "OrderedDict[tuple, LayerPlan]" = OrderedDict()
+_PLAN_CACHE_MAX = 64
+
+
+def plan_for_assignment(assignment, layout: TokenLayout) -> LayerPlan:
+    """Cached native plan for (layout, per-head specs).  The reference rebuilds
+    every mask on every call (attention.py:178-182); the plan is immutable, so
+    one build per distinct assignment suffices."""
+    key = (layout, tuple(assignment))
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        plan = LayerPlan.from_specs(list(assignment), layout)
+        _PLAN_CACHE[key] = plan
+        while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
+            _PLAN_CACHE.popitem(last=False)
+    else:
+        _PLAN_CACHE.move_to_end(key)
+    return plan
+
+
+# ---------------------------------------------------------------- tensors
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _check_qkv(q, k, v):
+    """Rank-4 and equal shapes (attention.py:27-33 / numerics.py:46-53)."""
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        nd = t.dim() if _is_torch(t) else np.ndim(t)
+        if nd != 4:
+            raise ShapeError(f"{name} must have rank 4 [B, H, N, d], got rank {nd}")
+    sq, sk, sv = (tuple(t.shape) for t in (q, k, v))
+    if not (sq == sk == sv):
+        raise ShapeError(f"q/k/v shapes differ: {sq}, {sk}, {sv}")
+    return sq
+
+
+def _tensor_dim(d: int) -> int:
+    if d <= 64:
+        return 64
+    if d <= 128:
+        return 128
+    raise nat.NativeError(f"head_dim {d} unsupported by the sm_100a kernel (max 128)")
+
+
+def _to_device(xs):
+    """Stage q, k, v as bf16 CUDA tensors with a 64/128-wide unit-stride last dim.
+
+    Returns (tensors, was_numpy, device)."""
+    import torch
+    import torch.nn.functional as F
+
+    was_numpy = not _is_torch(xs[0])
+    if was_numpy:
+        if not torch.cuda.is_available():
+            raise nat.NativeError("a CUDA device is required: the sm_100a kernel has no CPU path")
+        dev = torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = xs[0].device
+        if dev.type != "cuda":
+            raise nat.NativeError("tensors must live on a CUDA device (no CPU path)")
+    out = []
+    for x in xs:
+        if was_numpy:
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))
+            t = t.pin_memory().to(dev, non_blocking=True).to(torch.bfloat16)
+        else:
+            t = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
+        d = t.shape[-1]
+        dt = _tensor_dim(d)
+        if dt != d:
+            t = F.pad(t, (0, dt - d))
+        if t.stride(-1) != 1 or any((s * 2) % 16 for s in t.stride()[:-1]) or t.data_ptr() % 16:
+            t = t.contiguous()
+        out.append(t)
+    return out, was_numpy, dev
+
+
+def _run(plan: LayerPlan, q, k, v):
+    import torch
+
+    shape = _check_qkv(q, k, v)
+    B, H, N, d = shape
+    if plan.layout.total_tokens != N:
+        raise ShapeError(f"mask grid covers {plan.layout.total_tokens} tokens, tensors have {N}")
+    if plan.n_heads != H:
+        raise ConfigError(f"plan covers {plan.n_heads} heads, tensors have {H}")
+    (qt, kt, vt), was_numpy, dev = _to_device((q, k, v))
+    dt = qt.shape[-1]
+    out = torch.empty((B, H, N, dt), dtype=torch.bfloat16, device=dev)
+    plan.forward(qt, kt, vt, out, head_dim=d)
+    if dt != d:
+        out = out[..., :d]
+    if was_numpy:
+        res = out.float().cpu().numpy()
+        if not np.isfinite(res).all():
+            raise ShapeError("non-finite values in attention output")
+        return res
+    return out
+
+
+# ---------------------------------------------------------------- reference API
+
+
+@dataclass(frozen=True, eq=False)
+class HeadGroup:
+    """Heads of one layer sharing a pattern (attention.py:149-161)."""
+
+    spec: PatternSpec
+    heads: tuple[int, ...]
+    mask: BlockMask | None
+    plan: LayerPlan | None = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        if not self.heads:
+            raise ConfigError("head group must contain at least one head")
+        if len(set(self.heads)) != len(self.heads):
+            raise ConfigError(f"duplicate heads in group: {self.heads}")
+
+
+_GROUP_CACHE: "OrderedDict[tuple, list]" = OrderedDict()
+
+
+def group_heads(assignment, grid: BlockGrid) -> list[HeadGroup]:
+    """Fuse same-pattern heads; groups in first-occurrence order (attention.py:164-183).
+
+    Grouping, masks and the kernel schedule come from the native plan builder;
+    the returned groups share that plan, so fused_layer_attention launches it
+    without rebuilding anything."""
+    assignment = list(assignment)
+    key = (grid.layout, tuple(assignment))
+    cached = _GROUP_CACHE.get(key)
+    if cached is not None:
+        _GROUP_CACHE.move_to_end(key)
+        return list(cached)
+    plan = plan_for_assignment(assignment, grid.layout)
+    groups = []
+    for g in range(plan.info.n_groups):
+        heads, skip = plan.group_heads(g)
+        spec = assignment[heads[0]]
+        mask = None
+        if spec.mode not in (Mode.FULL, Mode.SKIP):
+            mask = BlockMask(grid=grid, active=plan.group_mask(g))
+        groups.append(HeadGroup(spec=spec, heads=heads, mask=mask, plan=plan))
+    _GROUP_CACHE[key] = groups
+    while len(_GROUP_CACHE) > _PLAN_CACHE_MAX:
+        _GROUP_CACHE.popitem(last=False)
+    return list(groups)
+
+
+def _plan_for_groups(groups, H: int, N: int) -> LayerPlan:
+    plans = {id(g.plan) for g in groups}
+    first = groups[0].plan
+    if len(plans) == 1 and first is not None and first.n_heads == H:
+        # the groups came from one group_heads() call: check they are that plan's
+        info = first.info
+        if info.n_groups == len(groups) and all(
+                first.group_heads(i)[0] == g.heads for i, g in enumerate(groups)):
+            return first
+    # hand-built groups: lower their masks explicitly
+    layout = None
+    masks, head_group = [], np.zeros(H, dtype=np.int32)
+    for gi, g in enumerate(groups):
+        if g.mask is not None:
+            layout = g.mask.grid.layout
+        if g.spec.mode is Mode.SKIP:
+            masks.append(None)
+        elif g.spec.mode is Mode.FULL or g.mask is None:
+            masks.append("full")
+        else:
+            masks.append(g.mask.active)
+        for h in g.heads:
+            head_group[h] = gi
+    if layout is None:
+        layout = _dense_layout(N)
+    nb = layout.n_blocks
+    masks = [np.ones((nb, nb), dtype=bool) if isinstance(m, str) else m for m in masks]
+    return LayerPlan.from_masks(layout, masks, head_group)
+
+
+def fused_layer_attention(q, k, v, groups):
+    """One layer's attention, every head in one kernel launch (attention.py:186-212)."""
+    B, H, N, d = _check_qkv(q, k, v)
+    seen: list[int] = []
+    for g in groups:
+        seen.extend(g.heads)
+    if sorted(seen) != list(range(H)):
+        raise ConfigError(f"groups cover heads {sorted(seen)}, tensors have {H} heads")
+    for g in groups:
+        if g.mask is not None and g.mask.grid.layout.total_tokens != N:
+            raise ShapeError(
+                f"mask grid covers {g.mask.grid.layout.total_tokens} tokens, tensors have {N}")
+    return _run(_plan_for_groups(groups, H, N), q, k, v)
+
+
+_MASK_PLANS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def sparse_attention(q, k, v, mask: BlockMask):
+    """Block-sparse attention restricted to `mask` (attention.py:57-98)."""
+    B, H, N, d = _check_qkv(q, k, v)
+    if mask.grid.layout.total_tokens != N:
+        raise ShapeError(f"mask grid covers {mask.grid.layout.total_tokens} tokens, tensors have {N}")
+    if mask.is_skip:
+        raise DegenerateRowError("skip mask defines no softmax; use skip_attention")
+    if not np.asarray(mask.active).any(axis=1).all():
+        raise DegenerateRowError("mask has a query row with no active key blocks")
+    per_mask = _MASK_PLANS.setdefault(mask, {})
+    plan = per_mask.get(H)
+    if plan is None:
+        plan = LayerPlan.from_masks(mask.grid.layout, [mask.active], np.zeros(H, dtype=np.int32))
+        per_mask[H] = plan
+    return _run(plan, q, k, v)
+
+
+def full_mask_attention(q, k, v, grid: BlockGrid):
+    """The streaming kernel with every block active (attention.py:101-105)."""
+    H = _check_qkv(q, k, v)[1]
+    return _run(plan_for_assignment([full_spec()] * H, grid.layout), q, k, v)
+
+
+def _dense_layout(n: int) -> TokenLayout:
+    return TokenLayout(text_tokens=0, frames=1, tokens_per_frame=n, block_size=64)
+
+
+def dense_attention(q, k, v):
+    """softmax(q k^T / sqrt(d)) v (attention.py:36-41) — the all-active kernel;
+    no [N, N] score matrix is materialised."""
+    B, H, N, d = _check_qkv(q, k, v)
+    return _run(plan_for_assignment([full_spec()] * H, _dense_layout(N)), q, k, v)
+
+
+def skip_attention(q, k, v):
+    """SKIP mode: exact zeros, zero FLOPs (attention.py:51-54)."""
+    B, H, N, d = _check_qkv(q, k, v)
+    return _run(plan_for_assignment([skip_spec()] * H, _dense_layout(N)), q, k, v)
+
+
+__all__ = [
+    "LayerPlan", "HeadGroup", "group_heads", "fused_layer_attention", "sparse_attention",
+    "full_mask_attention", "dense_attention", "skip_attention", "plan_for_assignment",
+]

@@ -1,0 +1,81 @@
+"""FLOP accounting (the reference convention) plus the B200 latency model.
+
+attention_flops / layer_linear_flops / attention_latency_share restate
+costmodel.py:26-50 with unchanged signatures and results, so the search's
+cost-model plugin surface stays intact.  `B200LatencyModel` is the re-fit
+of that model to measured per-pattern latencies of the sm_100a kernel
+(BASELINE config 5): it maps (mode, density, N, d, H) -> ms and exposes an
+"effective sparsity" 1 - t/t_full that plugs into mode_loss's sparsity slot.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+from pathlib import Path
+
+from .errors import ConfigError
+
+
+def attention_flops(n_tokens: int, head_dim: int, heads: int, sparsity: float) -> float:
+    """heads * (1 - sparsity) * 4 * N^2 * d (costmodel.py:26-32)."""
+    if n_tokens < 1 or head_dim < 1 or heads < 1:
+        raise ConfigError("n_tokens, head_dim, heads must all be >= 1")
+    if not 0.0 <= sparsity <= 1.0:
+        raise ConfigError(f"sparsity must be in [0, 1], got {sparsity}")
+    return heads * (1.0 - sparsity) * 4.0 * float(n_tokens) ** 2 * head_dim
+
+
+def layer_linear_flops(n_tokens: int, dim: int, ffn_mult: int = 4) -> float:
+    """Projections + MLP matmul FLOPs of one block (costmodel.py:35-39)."""
+    if n_tokens < 1 or dim < 1 or ffn_mult < 1:
+        raise ConfigError("n_tokens, dim, ffn_mult must all be >= 1")
+    return 8.0 * n_tokens * float(dim) ** 2 + 4.0 * ffn_mult * n_tokens * float(dim) ** 2
+
+
+def attention_latency_share(n_tokens: int, head_dim: int, heads: int, ffn_mult: int = 4) -> float:
+    """Dense attention's share of per-layer matmul FLOPs (costmodel.py:42-50)."""
+    attn = attention_flops(n_tokens, head_dim, heads, 0.0)
+    other = layer_linear_flops(n_tokens, heads * head_dim, ffn_mult)
+    return attn / (attn + other)
+
+
+@dataclass
+class B200LatencyModel:
+    """Measured latency model of the fused sm_100a layer kernel.
+
+    t(ms) = launch_ms + tiles * ms_per_tile(d), where `tiles` is the number of
+    128x128 MMA tiles the plan issues (LayerPlan.info.computed_tiles) — the
+    quantity the kernel's time is linear in.  Coefficients are fitted from
+    the config-5 sweep (bench.py --sweep) and stored as JSON.
+    """
+
+    launch_ms: float = 0.01
+    ms_per_tile: dict = field(default_factory=lambda: {64: 5.0e-6, 128: 8.0e-6})
+    source: str = "placeholder (not yet fitted)"
+
+    def predict_ms(self, computed_tiles: int, head_dim: int) -> float:
+        per = self.ms_per_tile.get(int(head_dim))
+        if per is None:
+            raise ConfigError(f"no latency fit for head_dim {head_dim}")
+        return self.launch_ms + computed_tiles * per
+
+    def effective_sparsity(self, computed_tiles: int, full_tiles: int, head_dim: int) -> float:
+        """1 - t(pattern) / t(full): the latency-weighted sparsity for mode_loss."""
+        t = self.predict_ms(computed_tiles, head_dim)
+        t_full = self.predict_ms(full_tiles, head_dim)
+        return min(1.0, max(0.0, 1.0 - t / t_full))
+
+    def save(self, path) -> None:
+        Path(path).write_text(json.dumps({
+            "launch_ms": self.launch_ms,
+            "ms_per_tile": {str(k): v for k, v in self.ms_per_tile.items()},
+            "source": self.source,
+        }, indent=2) + "\n")
+
+    @classmethod
+    def load(cls, path) -> "B200LatencyModel":
+        obj = json.loads(Path(path).read_text())
+        return cls(launch_ms=float(obj["launch_ms"]),
+                   ms_per_tile={int(k): float(v) for k, v in obj["ms_per_tile"].items()},
+                   source=obj.get("source", str(path)))

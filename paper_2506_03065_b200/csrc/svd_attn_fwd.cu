@@ -1,0 +1,605 @@
+// sm_100a block-sparse attention forward for the Sparse-vDiT hot path.
+//
+// Reference semantics: attention.py:57-98 (sparse_attention: per query block,
+// an online softmax over that block's active key blocks), attention.py:101-105
+// (full_mask_attention = all blocks active), attention.py:51-54 (skip: zeros)
+// and attention.py:186-212 (fused_layer_attention: every head of the layer in
+// one call, heads dispatched by pattern group).  Here the whole layer is ONE
+// launch: a CTA per work item (four 64-token query segments of one head that
+// share a list of 128-key tiles), heaviest items first.
+//
+// CTA anatomy (384 threads, 1 CTA / SM):
+//   warp 0       TMA producer: Q tiles once, then K and V tiles through two
+//                separate smem rings (SWIZZLE_128B boxes of 64x64 bf16)
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 4-7    softmax/epilogue for Q tile A (thread = row = TMEM lane)
+//   warps 8-11   softmax/epilogue for Q tile B
+// Per KV tile j the issuer runs, ping-ponging between the two Q tiles,
+//   S_X = Q_X K_j^T          (SS MMA, M=128 N=128 K=d, fp32 in TMEM)
+//   O_X += P_X V_j           (TS MMA: P bf16 from TMEM, V MN-major in smem)
+// while the softmax warpgroups turn S_X into P_X (masking, running max with
+// lazy rescale of O, exp2, row sums) — so one tile's exp overlaps the other
+// tile's MMAs.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "svd_plan.h"
+#include "svd_ptx.cuh"
+
+namespace svd {
+
+constexpr int kThreads = 384;
+constexpr uint32_t kTmemCols = 512;
+
+template <int D>
+struct KCfg {
+  static constexpr int kSlabs = D / 64;
+  static constexpr int kBoxBytes = 64 * 64 * 2;        // one TMA box: 64 rows x 128 B
+  static constexpr int kSlabBytes = 128 * 128;         // 128 rows x 128 B (one SW128 slab)
+  static constexpr int kTileBytes = 128 * D * 2;       // a Q tile or a KV tile
+  static constexpr int kKSt = D == 128 ? 2 : 4;
+  static constexpr int kVSt = D == 128 ? 2 : 4;
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + 2 * kTileBytes;
+  static constexpr int kOffV = kOffK + kKSt * kTileBytes;
+  static constexpr int kOffBar = kOffV + kVSt * kTileBytes;
+  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p[2] o[2]
+  static constexpr int kBarQ = 0;
+  static constexpr int kBarKF = 1;
+  static constexpr int kBarKE = kBarKF + kKSt;
+  static constexpr int kBarVF = kBarKE + kKSt;
+  static constexpr int kBarVE = kBarVF + kVSt;
+  static constexpr int kBarS = kBarVE + kVSt;
+  static constexpr int kBarP = kBarS + 2;
+  static constexpr int kBarO = kBarP + 2;
+  static constexpr int kNumBars = kBarO + 2;
+  static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
+  static constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
+  // TMEM columns.  d=128 uses all 512: P_X aliases the first 64 columns of S_X.
+  __device__ static constexpr uint32_t col_s(int x) { return x ? 128u : 0u; }
+  __device__ static constexpr uint32_t col_o(int x) { return x ? 256u + D : 256u; }
+  __device__ static constexpr uint32_t col_p(int x) {
+    return D == 128 ? col_s(x) : (x ? 448u : 384u);
+  }
+};
+
+struct FwdParams {
+  const WorkItem* items;
+  const KvEntry* kv;
+  const uint32_t* bits;      // fine-mask tables
+  const int64_t* bit_off;    // per group word offset
+  __nv_bfloat16* o;
+  int64_t o_sb, o_sh, o_sn;  // element strides of O (d stride is 1)
+  int n_tokens;
+  int block_size;
+  int words_per_row;
+  int n_blocks;
+  int packed;                // shard plan: O is a packed [rows, d] buffer
+  float scale_log2;          // log2(e) / sqrt(d)
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int D>
+__device__ __forceinline__ void load_tile(const CUtensorMap* tmap, uint32_t dst, uint32_t bar,
+                                          int seg0, int seg1, int head, int b, uint64_t pol) {
+  using C = KCfg<D>;
+#pragma unroll
+  for (int slot = 0; slot < 2; ++slot) {
+    const int seg = slot ? seg1 : seg0;
+#pragma unroll
+    for (int slab = 0; slab < C::kSlabs; ++slab)
+      ptx::tma_load_4d(dst + slab * C::kSlabBytes + slot * C::kBoxBytes, tmap, bar, slab * 64,
+                       seg * kSeg, head, b, pol);
+  }
+}
+
+// Mask one 128-key tile of S for this thread's row.
+__device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, int qslot, int tok_r,
+                                           const FwdParams& p, const uint32_t* bits_row) {
+  const bool on0 = (e.flags >> (2 * qslot)) & 1u;
+  const bool on1 = (e.flags >> (2 * qslot + 1)) & 1u;
+  const int lim0 = on0 ? min(kSeg, p.n_tokens - e.kseg0 * kSeg) : 0;
+  const int lim1 = (on1 && e.kseg1 >= 0) ? min(kSeg, p.n_tokens - e.kseg1 * kSeg) : 0;
+  if (e.flags & kFlagFine) {
+    // block_size % 64 != 0: the (query block, key block) bit of every element
+#pragma unroll
+    for (int i = 0; i < 128; ++i) {
+      const int slot = i >> 6;
+      const int lim = slot ? lim1 : lim0;
+      const int c = (slot ? e.kseg1 : e.kseg0) * kSeg + (i & 63);
+      bool ok = (i & 63) < lim;
+      if (ok) {
+        const int kb = c / p.block_size;
+        ok = (__ldg(bits_row + (kb >> 5)) >> (kb & 31)) & 1u;
+      }
+      if (!ok) s[i] = -INFINITY;
+    }
+    (void)tok_r;
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    if (i >= lim0) s[i] = -INFINITY;
+    if (i >= lim1) s[64 + i] = -INFINITY;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    svd_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  using C = KCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* base_ptr = smem_raw + (base - raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  auto bar = [&](int i) { return base + C::kOffBar + 8u * uint32_t(i); };
+
+  const WorkItem item = p.items[blockIdx.x];
+  const int b = blockIdx.y;
+  const int n_kv = item.kv_count;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(bar(C::kBarQ), 1);
+    for (int i = 0; i < C::kKSt; ++i) {
+      ptx::mbar_init(bar(C::kBarKF + i), 1);
+      ptx::mbar_init(bar(C::kBarKE + i), 1);
+    }
+    for (int i = 0; i < C::kVSt; ++i) {
+      ptx::mbar_init(bar(C::kBarVF + i), 1);
+      ptx::mbar_init(bar(C::kBarVE + i), 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(bar(C::kBarS + x), 1);
+      ptx::mbar_init(bar(C::kBarP + x), 128);
+      ptx::mbar_init(bar(C::kBarO + x), 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(base + C::kOffTmemSlot, kTmemCols);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(base_ptr + C::kOffTmemSlot);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && n_kv > 0) {
+      ptx::prefetch_tmap(&tm_q);
+      ptx::prefetch_tmap(&tm_k);
+      ptx::prefetch_tmap(&tm_v);
+      const uint64_t pol_q = ptx::policy_evict_first();
+      const uint64_t pol_kv = ptx::policy_evict_last();
+      int first = item.qseg[0];
+      ptx::mbar_arrive_expect_tx(bar(C::kBarQ), 2 * C::kTileBytes);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        int s0 = item.qseg[2 * x], s1 = item.qseg[2 * x + 1];
+        s0 = s0 >= 0 ? s0 : first;
+        s1 = s1 >= 0 ? s1 : first;
+        load_tile<D>(&tm_q, base + C::kOffQ + x * C::kTileBytes, bar(C::kBarQ), s0, s1, item.head,
+                     b, pol_q);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        const KvEntry e = p.kv[item.kv_begin + j];
+        const int k0 = e.kseg0, k1 = e.kseg1 >= 0 ? e.kseg1 : e.kseg0;
+        const int ks = j % C::kKSt, vs = j % C::kVSt;
+        ptx::mbar_wait(bar(C::kBarKE + ks), ((j / C::kKSt) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(bar(C::kBarKF + ks), C::kTileBytes);
+        load_tile<D>(&tm_k, base + C::kOffK + ks * C::kTileBytes, bar(C::kBarKF + ks), k0, k1,
+                     item.head, b, pol_kv);
+        ptx::mbar_wait(bar(C::kBarVE + vs), ((j / C::kVSt) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(bar(C::kBarVF + vs), C::kTileBytes);
+        load_tile<D>(&tm_v, base + C::kOffV + vs * C::kTileBytes, bar(C::kBarVF + vs), k0, k1,
+                     item.head, b, pol_kv);
+      }
+    }
+    __syncwarp();
+    return;
+  }
+
+  if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && n_kv > 0) {
+      constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false);
+      constexpr uint32_t id_pv = ptx::idesc_bf16(128, D, true);
+      auto issue_s = [&](int x, int ks) {
+        const uint32_t qb = base + C::kOffQ + x * C::kTileBytes;
+        const uint32_t kb = base + C::kOffK + ks * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
+          ptx::mma_ss(tmem + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
+                      ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
+        }
+      };
+      auto issue_pv = [&](int x, int vs, bool acc) {
+        const uint32_t vb = base + C::kOffV + vs * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_ts(tmem + C::col_o(x), tmem + C::col_p(x) + kk * 8,
+                      ptx::sw128_desc(vb + kk * 2048, C::kSlabBytes, 1024), id_pv,
+                      (acc || kk > 0) ? 1u : 0u);
+      };
+      ptx::mbar_wait(bar(C::kBarQ), 0);
+      ptx::mbar_wait(bar(C::kBarKF + 0), 0);
+      ptx::tc_fence_after();
+      issue_s(0, 0);
+      ptx::mma_commit(bar(C::kBarS + 0));
+      issue_s(1, 0);
+      ptx::mma_commit(bar(C::kBarS + 1));
+      ptx::mma_commit(bar(C::kBarKE + 0));
+      for (int j = 0; j < n_kv; ++j) {
+        const int vs = j % C::kVSt;
+        const int ks1 = (j + 1) % C::kKSt;
+        const bool more = j + 1 < n_kv;
+        ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
+        // tile A
+        ptx::mbar_wait(bar(C::kBarP + 0), j & 1);
+        ptx::tc_fence_after();
+        issue_pv(0, vs, j > 0);
+        if (!more) ptx::mma_commit(bar(C::kBarO + 0));
+        if (more) {
+          ptx::mbar_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1);
+          ptx::tc_fence_after();
+          issue_s(0, ks1);
+          ptx::mma_commit(bar(C::kBarS + 0));
+        }
+        // tile B
+        ptx::mbar_wait(bar(C::kBarP + 1), j & 1);
+        ptx::tc_fence_after();
+        issue_pv(1, vs, j > 0);
+        ptx::mma_commit(bar(C::kBarVE + vs));
+        if (!more) ptx::mma_commit(bar(C::kBarO + 1));
+        if (more) {
+          issue_s(1, ks1);
+          ptx::mma_commit(bar(C::kBarS + 1));
+          ptx::mma_commit(bar(C::kBarKE + ks1));
+        }
+      }
+    }
+    __syncwarp();
+    named_bar_sync(1, 32 + 256);
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kTmemCols);
+    return;
+  }
+
+  if (warp < 4) return;  // warps 2-3: no role
+
+  // -------------------------------------------------------------- softmax / epilogue
+  const int x = (warp - 4) >> 2;           // Q tile A (0) or B (1)
+  const int wq = warp & 3;                 // TMEM lane quarter
+  const int row = wq * 32 + lane;          // row of the 128-row tile
+  const uint32_t lane_off = uint32_t(wq * 32) << 16;
+  const int qslot = 2 * x + (row >> 6);
+  const int qseg = item.qseg[qslot];
+  const int tok_r = qseg * kSeg + (row & 63);
+  const bool row_valid = qseg >= 0 && tok_r < p.n_tokens;
+  __nv_bfloat16* orow;
+  if (p.packed)
+    orow = p.o + (int64_t(item.out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
+  else
+    orow = p.o + int64_t(b) * p.o_sb + int64_t(item.head) * p.o_sh + int64_t(tok_r) * p.o_sn;
+
+  if (n_kv == 0) {
+    // SKIP head (attention.py:51-54): exact zeros, no scores, no softmax
+    if (row_valid) {
+      uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) reinterpret_cast<uint4*>(orow)[c] = z;
+    }
+    named_bar_sync(1, 32 + 256);
+    return;
+  }
+
+  const uint32_t* bits_row = nullptr;
+  if (p.bits != nullptr) {
+    const int qb = min(max(tok_r, 0) / p.block_size, p.n_blocks - 1);
+    bits_row = p.bits + p.bit_off[item.group] + int64_t(qb) * p.words_per_row;
+  }
+  const float sl2 = p.scale_log2;
+  float m = -INFINITY;  // running max (log2 domain); lazily updated
+  float l = 0.f;        // running denominator relative to m
+
+  for (int j = 0; j < n_kv; ++j) {
+    ptx::mbar_wait(bar(C::kBarS + x), j & 1);
+    ptx::tc_fence_after();
+    float s[128];
+    const uint32_t ts = tmem + lane_off + C::col_s(x);
+    ptx::tmem_ld32(ts + 0, *reinterpret_cast<float(*)[32]>(&s[0]));
+    ptx::tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+    ptx::tmem_ld32(ts + 64, *reinterpret_cast<float(*)[32]>(&s[64]));
+    ptx::tmem_ld32(ts + 96, *reinterpret_cast<float(*)[32]>(&s[96]));
+    const KvEntry e = p.kv[item.kv_begin + j];
+    ptx::tmem_wait_ld();
+    if (!(e.flags & kFlagAll)) apply_mask(s, e, qslot, tok_r, p, bits_row);
+
+    float mx = s[0];
+#pragma unroll
+    for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+    const float m_new = fmaxf(m, mx * sl2);
+    // lazy rescale: keep a stale max unless it grew by more than 2^8
+    const bool resc = m_new > m + 8.0f;
+    if (__any_sync(0xffffffffu, resc)) {
+      const float alpha = resc ? ptx::ex2(m - m_new) : 1.0f;
+      if (j > 0) {
+        const uint32_t to = tmem + lane_off + C::col_o(x);
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float ov[32];
+          ptx::tmem_ld32(to + c * 32, ov);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] *= alpha;
+          ptx::tmem_st32(to + c * 32, ov);
+        }
+      }
+      if (resc) {
+        l *= alpha;
+        m = m_new;
+      }
+    }
+    const float mref = (m == -INFINITY) ? 0.f : m;
+    const uint32_t tp = tmem + lane_off + C::col_p(x);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float p0 = ptx::ex2(fmaf(s[c * 32 + 2 * i], sl2, -mref));
+        const float p1 = ptx::ex2(fmaf(s[c * 32 + 2 * i + 1], sl2, -mref));
+        l += p0 + p1;
+        pk[i] = ptx::pack_bf16(p0, p1);
+      }
+      ptx::tmem_st16(tp + c * 16, pk);
+    }
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    ptx::mbar_arrive(bar(C::kBarP + x));
+  }
+
+  // epilogue: O / l -> bf16 rows
+  ptx::mbar_wait(bar(C::kBarO + x), 0);
+  ptx::tc_fence_after();
+  const float inv = l > 0.f ? 1.0f / l : 0.f;
+  const uint32_t to = tmem + lane_off + C::col_o(x);
+#pragma unroll
+  for (int c = 0; c < D / 32; ++c) {
+    float ov[32];
+    ptx::tmem_ld32(to + c * 32, ov);
+    ptx::tmem_wait_ld();
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
+    if (row_valid) {
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+    }
+  }
+  ptx::tc_fence_before();
+  named_bar_sync(1, 32 + 256);
+}
+
+// Multi-GPU reassembly: packed shard rows -> O[0, head, token, :]
+__global__ void svd_unpack_kernel(const int32_t* __restrict__ row_head,
+                                  const int32_t* __restrict__ row_token, int64_t n_rows,
+                                  const __nv_bfloat16* __restrict__ packed, int64_t prs,
+                                  __nv_bfloat16* __restrict__ o, int64_t o_sh, int64_t o_sn,
+                                  int vec_per_row) {
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r = gid / vec_per_row;
+  const int c = int(gid % vec_per_row);
+  if (r >= n_rows) return;
+  const int h = row_head[r];
+  if (h < 0) return;
+  const int t = row_token[r];
+  const uint4 v = reinterpret_cast<const uint4*>(packed + r * prs)[c];
+  reinterpret_cast<uint4*>(o + int64_t(h) * o_sh + int64_t(t) * o_sn)[c] = v;
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int make_tmap(CUtensorMap* map, const void* ptr, const int64_t* st, int64_t B, int64_t H,
+                     int64_t N, int D, const char* name) {
+  auto enc = get_encode_fn();
+  if (!enc) return fail(SVD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if (st[3] != 1) return fail(SVD_ERR_UNSUPPORTED, std::string(name) + ": head_dim stride must be 1");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0)
+    return fail(SVD_ERR_UNSUPPORTED, std::string(name) + ": base pointer not 16-byte aligned");
+  cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(N), cuuint64_t(H), cuuint64_t(B)};
+  cuuint64_t strides[3] = {cuuint64_t(st[2] * 2), cuuint64_t(st[1] * 2), cuuint64_t(st[0] * 2)};
+  for (int i = 0; i < 3; ++i)
+    if (strides[i] % 16 != 0 && dims[i + 1] > 1)
+      return fail(SVD_ERR_UNSUPPORTED, std::string(name) + ": strides must be 16-byte multiples");
+  for (int i = 0; i < 3; ++i)
+    if (dims[i + 1] == 1) strides[i] = std::max<cuuint64_t>(strides[i], 16) / 16 * 16;
+  cuuint32_t box[4] = {64, 64, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SVD_ERR_CUDA, std::string(name) + ": cuTensorMapEncodeTiled failed (" +
+                                  std::to_string(int(r)) + ")");
+  return SVD_OK;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SVD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int ensure_device_tables(const svd_plan* P, DeviceTables** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(P->mu);
+  auto it = P->dev.find(dev);
+  if (it != P->dev.end()) {
+    *out = &it->second;
+    return SVD_OK;
+  }
+  DeviceTables t;
+  auto upload = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+    if (bytes == 0) bytes = 16;
+    cudaError_t err = cudaMalloc(dst, bytes);
+    if (err != cudaSuccess) return err;
+    if (src) return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    return cudaMemset(*dst, 0, bytes);
+  };
+  if ((e = upload(&t.items, P->items.data(), P->items.size() * sizeof(WorkItem))) != cudaSuccess ||
+      (e = upload(&t.kv, P->kv.empty() ? nullptr : P->kv.data(), P->kv.size() * sizeof(KvEntry))) !=
+          cudaSuccess ||
+      (e = upload(&t.bits, P->fine_bits.empty() ? nullptr : P->fine_bits.data(),
+                  P->fine_bits.size() * 4)) != cudaSuccess ||
+      (e = upload(&t.bit_off, P->fine_bit_off.data(), P->fine_bit_off.size() * 8)) != cudaSuccess)
+    return cuda_fail(e, "plan upload");
+  t.n_items = int64_t(P->items.size());
+  auto res = P->dev.emplace(dev, t);
+  *out = &res.first->second;
+  return SVD_OK;
+}
+
+void release_device_tables(const svd_plan* P) {
+  std::lock_guard<std::mutex> lock(P->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : P->dev) {
+    cudaSetDevice(kv.first);
+    cudaFree(kv.second.items);
+    cudaFree(kv.second.kv);
+    cudaFree(kv.second.bits);
+    cudaFree(kv.second.bit_off);
+  }
+  P->dev.clear();
+  cudaSetDevice(cur);
+}
+
+template <int D>
+static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const void* k,
+                      const void* v, void* o, const int64_t* qs, const int64_t* ks,
+                      const int64_t* vs, const int64_t* os, int32_t batch, int32_t head_dim,
+                      cudaStream_t stream) {
+  using C = KCfg<D>;
+  CUtensorMap mq, mk, mv;
+  const int64_t N = P->grid.n, H = P->n_heads;
+  int st;
+  if ((st = make_tmap(&mq, q, qs, batch, H, N, D, "q"))) return st;
+  if ((st = make_tmap(&mk, k, ks, batch, H, N, D, "k"))) return st;
+  if ((st = make_tmap(&mv, v, vs, batch, H, N, D, "v"))) return st;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(svd_fwd_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_set[dev] = true;
+  }
+  FwdParams prm{};
+  prm.items = static_cast<const WorkItem*>(T->items);
+  prm.kv = static_cast<const KvEntry*>(T->kv);
+  prm.bits = P->fine ? static_cast<const uint32_t*>(T->bits) : nullptr;
+  prm.bit_off = static_cast<const int64_t*>(T->bit_off);
+  prm.o = static_cast<__nv_bfloat16*>(o);
+  prm.o_sb = os[0];
+  prm.o_sh = os[1];
+  prm.o_sn = os[2];
+  prm.n_tokens = int(N);
+  prm.block_size = int(P->grid.bs);
+  prm.words_per_row = int((P->grid.nb + 31) / 32);
+  prm.n_blocks = int(P->grid.nb);
+  prm.packed = P->sharded ? 1 : 0;
+  prm.scale_log2 = float(1.4426950408889634 / std::sqrt(double(head_dim)));
+  if (T->n_items == 0) return SVD_OK;
+  dim3 grid(unsigned(T->n_items), unsigned(batch));
+  svd_fwd_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "svd_fwd_kernel launch");
+  return SVD_OK;
+}
+
+}  // namespace svd
+
+using namespace svd;
+
+extern "C" {
+
+const char* svd_version(void) { return "svdit_b200 0.1.0 sm_100a tcgen05/TMA"; }
+
+int svd_attn_fwd(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
+                 const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                 const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                 int32_t dtype, void* stream) {
+  if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
+  if (dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
+  if (head_dim < 1 || head_dim > tensor_dim)
+    return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
+  if (batch < 1) return fail(SVD_ERR_SHAPE, "batch must be >= 1");
+  if (P->sharded && batch != 1) return fail(SVD_ERR_UNSUPPORTED, "shard plans run with batch 1");
+  if (!q || !k || !v || !o) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
+  if (o_strides[3] != 1 || (o_strides[2] * 2) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(o) & 15) != 0)
+    return fail(SVD_ERR_UNSUPPORTED, "o: rows must be contiguous and 16-byte aligned");
+  DeviceTables* T = nullptr;
+  int st = ensure_device_tables(P, &T);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (tensor_dim) {
+    case 64:
+      return launch_fwd<64>(P, T, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch,
+                            head_dim, s);
+    case 128:
+      return launch_fwd<128>(P, T, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch,
+                             head_dim, s);
+    default:
+      return fail(SVD_ERR_UNSUPPORTED,
+                  "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
+  }
+}
+
+int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, int64_t n_rows,
+                    const void* packed, int64_t packed_row_stride, void* o, const int64_t* o_strides,
+                    int32_t head_dim, void* stream) {
+  if (head_dim % 8 != 0) return fail(SVD_ERR_UNSUPPORTED, "head_dim must be a multiple of 8");
+  if (n_rows <= 0) return SVD_OK;
+  const int vec = head_dim / 8;
+  const int64_t total = n_rows * vec;
+  const int threads = 256;
+  const unsigned blocks = unsigned((total + threads - 1) / threads);
+  svd_unpack_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      row_head_dev, row_token_dev, n_rows, static_cast<const __nv_bfloat16*>(packed),
+      packed_row_stride, static_cast<__nv_bfloat16*>(o), o_strides[1], o_strides[2], vec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "svd_unpack_kernel launch");
+  return SVD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,645 @@
+// Host plan builder: block grid, pattern masks, head grouping and the
+// kernel's work schedule.  Everything integer here is bit-exact with the
+// reference (svdit 0.1.0):
+//   layout.py:26-80    TokenLayout validation, total_tokens, frame_of
+//   layout.py:135-158  block_grid (bounds / has_text / mixed / frame_index)
+//   patterns.py:334-339 frame_period (Python round(): half-to-even)
+//   patterns.py:377-417 build_mask (5 modes, forced rows/cols, empty-row error)
+//   attention.py:164-183 group_heads (first-occurrence order, ascending heads,
+//                         keyed on full PatternSpec equality)
+// and then lowers each group's block mask to the kernel schedule: 64-token
+// query segments clustered four to a CTA, each cluster with one ascending
+// list of 128-key tiles (pairs of key segments) plus per-tile activity bits.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "svd_plan.h"
+
+namespace svd {
+
+static thread_local std::string g_last_error = "";
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+bool NormSpec::operator<(const NormSpec& o) const {
+  auto key = [](const NormSpec& s) {
+    return std::make_tuple(s.mode, s.halfwidth, s.period, s.md_halfwidth, s.stripe_count,
+                           s.include_diagonal, s.stripes_none, s.stripes);
+  };
+  return key(*this) < key(o);
+}
+
+bool NormSpec::operator==(const NormSpec& o) const { return !(*this < o) && !(o < *this); }
+
+// ---------------------------------------------------------------- layout
+// layout.py:33-43 TokenLayout.__post_init__
+static int check_layout(const svd_layout* L) {
+  if (!L) return fail(SVD_ERR_CONFIG, "layout is NULL");
+  if (L->text_tokens < 0)
+    return fail(SVD_ERR_CONFIG, "text_tokens must be >= 0, got " + std::to_string(L->text_tokens));
+  if (L->frames < 0 || L->tokens_per_frame < 0)
+    return fail(SVD_ERR_CONFIG, "frames and tokens_per_frame must be >= 0");
+  if (L->frames > 0 && L->tokens_per_frame == 0)
+    return fail(SVD_ERR_CONFIG, "frames > 0 requires tokens_per_frame > 0");
+  if (L->block_size < 1)
+    return fail(SVD_ERR_CONFIG, "block_size must be >= 1, got " + std::to_string(L->block_size));
+  if (L->text_tokens + L->frames * L->tokens_per_frame < 1)
+    return fail(SVD_ERR_CONFIG, "layout has no tokens");
+  return SVD_OK;
+}
+
+// layout.py:57-63 frame_of (token already range-checked by callers)
+static inline int64_t frame_of(const svd_layout* L, int64_t token) {
+  if (token < L->text_tokens) return -1;
+  return (token - L->text_tokens) / L->tokens_per_frame;
+}
+
+// layout.py:135-158 block_grid
+static int make_grid(const svd_layout* L, Grid* g) {
+  int st = check_layout(L);
+  if (st) return st;
+  const int64_t n = L->text_tokens + L->frames * L->tokens_per_frame;
+  const int64_t size = L->block_size;
+  const int64_t nb = (n + size - 1) / size;
+  g->n = n;
+  g->nb = nb;
+  g->bs = size;
+  g->bounds.resize(nb + 1);
+  for (int64_t b = 0; b <= nb; ++b) g->bounds[b] = std::min(b * size, n);
+  g->has_text.assign(nb, 0);
+  g->mixed.assign(nb, 0);
+  g->frame_index.assign(nb, -1);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t t0 = g->bounds[b], t1 = g->bounds[b + 1];
+    g->has_text[b] = t0 < L->text_tokens;
+    const int64_t first_video = std::max(t0, L->text_tokens);
+    if (first_video < t1) {
+      g->frame_index[b] = frame_of(L, first_video);
+      const bool straddles = t0 < L->text_tokens;
+      const bool spans = frame_of(L, t1 - 1) != g->frame_index[b];
+      g->mixed[b] = straddles || spans;
+    }
+  }
+  return SVD_OK;
+}
+
+// patterns.py:334-339 frame_period: max(1, round(tpf / size)), banker's rounding
+static int64_t frame_period(const svd_layout* L) {
+  const double ratio = double(L->tokens_per_frame) / double(L->block_size);
+  const int64_t r = int64_t(std::nearbyint(ratio));  // FE_TONEAREST = half-to-even
+  return std::max<int64_t>(1, r);
+}
+
+// ---------------------------------------------------------------- specs
+// patterns.py:225-233 PatternSpec.__post_init__ (validation + stripe normalisation)
+static int normalise_spec(const svd_spec* s, NormSpec* out) {
+  if (!s) return fail(SVD_ERR_CONFIG, "spec is NULL");
+  if (s->mode < 0 || s->mode > 4)
+    return fail(SVD_ERR_CONFIG, "mode code must be in 0..4, got " + std::to_string(s->mode));
+  if (s->halfwidth < 0 || s->md_halfwidth < 0) return fail(SVD_ERR_CONFIG, "halfwidth must be >= 0");
+  if (s->stripe_count < 1)
+    return fail(SVD_ERR_CONFIG, "stripe_count must be >= 1, got " + std::to_string(s->stripe_count));
+  out->mode = s->mode;
+  out->halfwidth = s->halfwidth;
+  out->period = s->period > 0 ? s->period : -1;
+  out->md_halfwidth = s->md_halfwidth;
+  out->stripe_count = s->stripe_count;
+  out->include_diagonal = s->include_diagonal ? 1 : 0;
+  out->stripes_none = s->n_stripes < 0;
+  out->stripes.clear();
+  if (!out->stripes_none) {
+    if (s->n_stripes > 0 && !s->stripes) return fail(SVD_ERR_CONFIG, "stripes pointer is NULL");
+    out->stripes.assign(s->stripes, s->stripes + s->n_stripes);
+    std::sort(out->stripes.begin(), out->stripes.end());
+    out->stripes.erase(std::unique(out->stripes.begin(), out->stripes.end()), out->stripes.end());
+  }
+  return SVD_OK;
+}
+
+// patterns.py:377-417 build_mask.  active must hold nb*nb bytes.
+static int build_mask(const NormSpec& spec, const Grid& g, const svd_layout* L, uint8_t* active,
+                      bool* is_skip) {
+  const int64_t nb = g.nb;
+  *is_skip = false;
+  if (spec.mode == SVD_SKIP) {
+    *is_skip = true;
+    return SVD_OK;
+  }
+  if (spec.mode == SVD_FULL) {
+    std::memset(active, 1, size_t(nb * nb));
+    return SVD_OK;
+  }
+  if (spec.mode == SVD_DIAGONAL) {
+    const int64_t hw = spec.halfwidth;
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t j = 0; j < nb; ++j) active[i * nb + j] = std::llabs(i - j) <= hw;
+  } else if (spec.mode == SVD_MULTI_DIAGONAL) {
+    const int64_t period = spec.period > 0 ? spec.period : frame_period(L);
+    const int64_t hw = spec.md_halfwidth;
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t j = 0; j < nb; ++j) {
+        const int64_t folded = std::llabs(i - j) % period;
+        active[i * nb + j] = (folded <= hw) || (period - folded <= hw);
+      }
+  } else {  // VERTICAL_STRIPE
+    if (spec.stripes_none)
+      return fail(SVD_ERR_CONFIG,
+                  "vertical-stripe spec has no resolved stripe columns; pass stripes=... or let the "
+                  "search pick them");
+    std::memset(active, 0, size_t(nb * nb));
+    for (int64_t col : spec.stripes) {
+      if (!(0 <= col && col < nb))
+        return fail(SVD_ERR_CONFIG, "stripe column " + std::to_string(col) + " outside grid of " +
+                                        std::to_string(nb) + " blocks");
+      for (int64_t i = 0; i < nb; ++i) active[i * nb + col] = 1;
+    }
+    if (spec.include_diagonal)
+      for (int64_t i = 0; i < nb; ++i) active[i * nb + i] = 1;
+  }
+  // layout.py:119-122 forced = has_text | mixed; patterns.py:411-413
+  for (int64_t b = 0; b < nb; ++b) {
+    if (!(g.has_text[b] || g.mixed[b])) continue;
+    std::memset(active + b * nb, 1, size_t(nb));
+    for (int64_t i = 0; i < nb; ++i) active[i * nb + b] = 1;
+  }
+  // patterns.py:414-416
+  for (int64_t i = 0; i < nb; ++i) {
+    bool any = false;
+    for (int64_t j = 0; j < nb && !any; ++j) any = active[i * nb + j];
+    if (!any)
+      return fail(SVD_ERR_DEGENERATE_MASK,
+                  "query block " + std::to_string(i) + " has no active key blocks");
+  }
+  return SVD_OK;
+}
+
+// ---------------------------------------------------------------- schedule
+// Segment-level key sets of one group: keyset[s] bit ks is set when any
+// active (qb, kb) pair touches query segment s and key segment ks.
+static void segment_keysets(const Group& grp, const Grid& g, int64_t nseg,
+                            std::vector<std::vector<uint64_t>>* keyset) {
+  const int64_t nb = g.nb, bs = g.bs, n = g.n;
+  const int64_t words = (nseg + 63) / 64;
+  keyset->assign(nseg, std::vector<uint64_t>(words, 0));
+  std::vector<uint8_t> row(nb);
+  std::vector<int64_t> prefix(nb + 1);
+  for (int64_t s = 0; s < nseg; ++s) {
+    const int64_t t0 = s * kSeg, t1 = std::min(t0 + kSeg, n);
+    const int64_t b0 = t0 / bs, b1 = (t1 - 1) / bs;
+    std::fill(row.begin(), row.end(), 0);
+    for (int64_t b = b0; b <= b1; ++b)
+      for (int64_t j = 0; j < nb; ++j) row[j] |= grp.active[b * nb + j];
+    prefix[0] = 0;
+    for (int64_t j = 0; j < nb; ++j) prefix[j + 1] = prefix[j] + row[j];
+    auto& ks_bits = (*keyset)[s];
+    for (int64_t ks = 0; ks < nseg; ++ks) {
+      const int64_t c0 = ks * kSeg, c1 = std::min(c0 + kSeg, n);
+      const int64_t k0 = c0 / bs, k1 = (c1 - 1) / bs;
+      if (prefix[k1 + 1] - prefix[k0] > 0) ks_bits[ks >> 6] |= 1ull << (ks & 63);
+    }
+  }
+}
+
+static inline bool bit_of(const std::vector<uint64_t>& bits, int64_t i) {
+  return (bits[i >> 6] >> (i & 63)) & 1ull;
+}
+
+// Cluster query segments four to a CTA so that the four share (nearly) one key
+// set: identical key sets first (forced rows, FULL heads, multi-diagonal
+// residue classes), then the remainder in index order (diagonal bands and
+// stripes, whose neighbouring rows overlap).
+static std::vector<std::array<int32_t, kSlotsPerItem>> cluster_segments(
+    const std::vector<std::vector<uint64_t>>& keyset, int64_t nseg) {
+  std::map<std::vector<uint64_t>, std::vector<int32_t>> buckets;
+  std::vector<const std::vector<uint64_t>*> order;
+  for (int64_t s = 0; s < nseg; ++s) {
+    auto it = buckets.find(keyset[s]);
+    if (it == buckets.end()) {
+      it = buckets.emplace(keyset[s], std::vector<int32_t>()).first;
+      order.push_back(&it->first);
+    }
+    it->second.push_back(int32_t(s));
+  }
+  std::vector<std::array<int32_t, kSlotsPerItem>> out;
+  std::vector<int32_t> rest;
+  for (auto* key : order) {
+    const auto& members = buckets[*key];
+    size_t full = members.size() / kSlotsPerItem * kSlotsPerItem;
+    for (size_t i = 0; i < full; i += kSlotsPerItem) {
+      std::array<int32_t, kSlotsPerItem> q;
+      for (int k = 0; k < kSlotsPerItem; ++k) q[k] = members[i + k];
+      out.push_back(q);
+    }
+    for (size_t i = full; i < members.size(); ++i) rest.push_back(members[i]);
+  }
+  std::sort(rest.begin(), rest.end());
+  for (size_t i = 0; i < rest.size(); i += kSlotsPerItem) {
+    std::array<int32_t, kSlotsPerItem> q;
+    for (int k = 0; k < kSlotsPerItem; ++k) q[k] = i + k < rest.size() ? rest[i + k] : -1;
+    out.push_back(q);
+  }
+  return out;
+}
+
+static void build_group_schedule(svd_plan* P, Group& grp) {
+  const int64_t nseg = P->nseg;
+  grp.qgroups.clear();
+  grp.qgroup_kv_begin.clear();
+  grp.qgroup_kv_count.clear();
+  if (grp.skip) {
+    for (int64_t s = 0; s < nseg; s += kSlotsPerItem) {
+      std::array<int32_t, kSlotsPerItem> q;
+      for (int k = 0; k < kSlotsPerItem; ++k) q[k] = s + k < nseg ? int32_t(s + k) : -1;
+      grp.qgroups.push_back(q);
+      grp.qgroup_kv_begin.push_back(0);
+      grp.qgroup_kv_count.push_back(0);
+    }
+    return;
+  }
+  std::vector<std::vector<uint64_t>> keyset;
+  segment_keysets(grp, P->grid, nseg, &keyset);
+  grp.qgroups = cluster_segments(keyset, nseg);
+  const bool tail_partial = (P->grid.n % kSeg) != 0;
+  const int64_t words = (nseg + 63) / 64;
+  std::vector<uint64_t> uni(words);
+  for (auto& q : grp.qgroups) {
+    std::fill(uni.begin(), uni.end(), 0);
+    for (int k = 0; k < kSlotsPerItem; ++k)
+      if (q[k] >= 0)
+        for (int64_t w = 0; w < words; ++w) uni[w] |= keyset[q[k]][w];
+    std::vector<int32_t> keys;
+    for (int64_t ks = 0; ks < nseg; ++ks)
+      if (bit_of(uni, ks)) keys.push_back(int32_t(ks));
+    grp.qgroup_kv_begin.push_back(int32_t(P->kv.size()));
+    for (size_t i = 0; i < keys.size(); i += 2) {
+      KvEntry e{};
+      e.kseg0 = keys[i];
+      e.kseg1 = i + 1 < keys.size() ? keys[i + 1] : -1;
+      uint32_t bits = 0;
+      bool all = e.kseg1 >= 0 && !P->fine;
+      for (int slot = 0; slot < kSlotsPerItem; ++slot) {
+        for (int kslot = 0; kslot < 2; ++kslot) {
+          const int32_t ks = kslot == 0 ? e.kseg0 : e.kseg1;
+          bool on;
+          if (q[slot] < 0) on = true;  // empty q slot: never stored
+          else on = ks >= 0 && bit_of(keyset[q[slot]], ks);
+          if (on) bits |= 1u << (2 * slot + kslot);
+          else all = false;
+        }
+      }
+      const bool tail = tail_partial && (e.kseg0 == nseg - 1 || e.kseg1 == nseg - 1);
+      if (tail) all = false;
+      e.flags = bits | (all ? kFlagAll : 0u) | (tail ? kFlagTail : 0u) | (P->fine ? kFlagFine : 0u);
+      P->kv.push_back(e);
+    }
+    grp.qgroup_kv_count.push_back(int32_t(P->kv.size()) - grp.qgroup_kv_begin.back());
+  }
+}
+
+static double group_active_pairs(const Group& grp, const Grid& g) {
+  if (grp.skip) return 0.0;
+  const int64_t nb = g.nb;
+  double total = 0.0;
+  for (int64_t i = 0; i < nb; ++i) {
+    const double rows = double(g.bounds[i + 1] - g.bounds[i]);
+    double cols = 0.0;
+    for (int64_t j = 0; j < nb; ++j)
+      if (grp.active[i * nb + j]) cols += double(g.bounds[j + 1] - g.bounds[j]);
+    total += rows * cols;
+  }
+  return total;
+}
+
+static void finalize_plan(svd_plan* P) {
+  P->nseg = (P->grid.n + kSeg - 1) / kSeg;
+  P->fine = (P->grid.bs % kSeg) != 0;
+  P->kv.clear();
+  for (auto& grp : P->groups) build_group_schedule(P, grp);
+  // fine-mask bit tables (per element lookups when block_size % 64 != 0)
+  P->fine_bits.clear();
+  P->fine_bit_off.assign(P->groups.size(), -1);
+  if (P->fine) {
+    const int64_t nb = P->grid.nb, wpr = (nb + 31) / 32;
+    for (size_t gi = 0; gi < P->groups.size(); ++gi) {
+      const Group& grp = P->groups[gi];
+      if (grp.skip) continue;
+      P->fine_bit_off[gi] = int64_t(P->fine_bits.size());
+      P->fine_bits.resize(P->fine_bits.size() + size_t(nb * wpr), 0u);
+      uint32_t* base = P->fine_bits.data() + P->fine_bit_off[gi];
+      for (int64_t i = 0; i < nb; ++i)
+        for (int64_t j = 0; j < nb; ++j)
+          if (grp.active[i * nb + j]) base[i * wpr + (j >> 5)] |= 1u << (j & 31);
+    }
+  }
+  P->items.clear();
+  P->active_pairs = 0.0;
+  for (size_t gi = 0; gi < P->groups.size(); ++gi) {
+    const Group& grp = P->groups[gi];
+    P->active_pairs += double(grp.heads.size()) * group_active_pairs(grp, P->grid);
+    for (int32_t h : grp.heads) {
+      for (size_t qi = 0; qi < grp.qgroups.size(); ++qi) {
+        WorkItem it{};
+        it.head = h;
+        it.group = int32_t(gi);
+        it.kv_begin = grp.qgroup_kv_begin[qi];
+        it.kv_count = grp.qgroup_kv_count[qi];
+        for (int k = 0; k < kSlotsPerItem; ++k) it.qseg[k] = grp.qgroups[qi][k];
+        it.out_base = -1;
+        P->items.push_back(it);
+      }
+    }
+  }
+  // heaviest first: the hardware block scheduler then behaves like LPT
+  std::stable_sort(P->items.begin(), P->items.end(),
+                   [](const WorkItem& a, const WorkItem& b) { return a.kv_count > b.kv_count; });
+  P->computed_tiles = 0;
+  for (const auto& it : P->items) P->computed_tiles += 2 * int64_t(it.kv_count);
+}
+
+}  // namespace svd
+
+using namespace svd;
+
+extern "C" {
+
+const char* svd_last_error(void) { return g_last_error.c_str(); }
+
+int svd_grid_size(const svd_layout* layout, int64_t* n_tokens, int64_t* n_blocks) {
+  int st = check_layout(layout);
+  if (st) return st;
+  const int64_t n = layout->text_tokens + layout->frames * layout->tokens_per_frame;
+  if (n_tokens) *n_tokens = n;
+  if (n_blocks) *n_blocks = (n + layout->block_size - 1) / layout->block_size;
+  return SVD_OK;
+}
+
+int svd_grid_arrays(const svd_layout* layout, int64_t* bounds, uint8_t* has_text, uint8_t* mixed,
+                    int64_t* frame_index) {
+  Grid g;
+  int st = make_grid(layout, &g);
+  if (st) return st;
+  if (bounds) std::copy(g.bounds.begin(), g.bounds.end(), bounds);
+  if (has_text) std::copy(g.has_text.begin(), g.has_text.end(), has_text);
+  if (mixed) std::copy(g.mixed.begin(), g.mixed.end(), mixed);
+  if (frame_index) std::copy(g.frame_index.begin(), g.frame_index.end(), frame_index);
+  return SVD_OK;
+}
+
+int svd_frame_period(const svd_layout* layout, int64_t* period) {
+  int st = check_layout(layout);
+  if (st) return st;
+  *period = frame_period(layout);
+  return SVD_OK;
+}
+
+int svd_mask_build(const svd_layout* layout, const svd_spec* spec, uint8_t* active,
+                   int32_t* is_skip) {
+  Grid g;
+  int st = make_grid(layout, &g);
+  if (st) return st;
+  NormSpec ns;
+  st = normalise_spec(spec, &ns);
+  if (st) return st;
+  bool skip = false;
+  if (ns.mode == SVD_SKIP) {
+    if (is_skip) *is_skip = 1;
+    return SVD_OK;
+  }
+  if (!active) return fail(SVD_ERR_CONFIG, "active buffer is NULL");
+  st = build_mask(ns, g, layout, active, &skip);
+  if (is_skip) *is_skip = skip ? 1 : 0;
+  return st;
+}
+
+int svd_plan_create(const svd_layout* layout, const svd_spec* specs, int32_t n_heads,
+                    svd_plan** plan) {
+  if (!plan) return fail(SVD_ERR_CONFIG, "plan out-pointer is NULL");
+  *plan = nullptr;
+  if (n_heads < 1) return fail(SVD_ERR_CONFIG, "need at least one head");
+  if (!specs) return fail(SVD_ERR_CONFIG, "specs is NULL");
+  auto* P = new svd_plan();
+  P->layout = *layout;
+  int st = make_grid(layout, &P->grid);
+  if (st) {
+    delete P;
+    return st;
+  }
+  P->n_heads = n_heads;
+  // attention.py:170-176: first-occurrence order, members ascending
+  std::vector<NormSpec> norm(n_heads);
+  for (int32_t h = 0; h < n_heads; ++h) {
+    st = normalise_spec(&specs[h], &norm[h]);
+    if (st) {
+      delete P;
+      return st;
+    }
+  }
+  std::map<NormSpec, int32_t> index;
+  P->head_group.resize(n_heads);
+  for (int32_t h = 0; h < n_heads; ++h) {
+    auto it = index.find(norm[h]);
+    if (it == index.end()) {
+      it = index.emplace(norm[h], int32_t(P->groups.size())).first;
+      Group grp;
+      grp.spec = norm[h];
+      P->groups.push_back(std::move(grp));
+    }
+    P->groups[it->second].heads.push_back(h);
+    P->head_group[h] = it->second;
+  }
+  // attention.py:177-182: one mask per non-FULL/SKIP group, built in group order
+  const int64_t nb = P->grid.nb;
+  for (auto& grp : P->groups) {
+    grp.skip = grp.spec.mode == SVD_SKIP;
+    if (grp.skip) continue;
+    grp.active.assign(size_t(nb * nb), 0);
+    bool skip = false;
+    st = build_mask(grp.spec, P->grid, layout, grp.active.data(), &skip);
+    if (st) {
+      delete P;
+      return st;
+    }
+  }
+  finalize_plan(P);
+  *plan = P;
+  return SVD_OK;
+}
+
+int svd_plan_create_from_masks(const svd_layout* layout, int32_t n_groups, const int32_t* group_skip,
+                               const uint8_t* masks, const int32_t* head_group, int32_t n_heads,
+                               svd_plan** plan) {
+  if (!plan) return fail(SVD_ERR_CONFIG, "plan out-pointer is NULL");
+  *plan = nullptr;
+  if (n_heads < 1 || n_groups < 1) return fail(SVD_ERR_CONFIG, "need at least one head and group");
+  if (!masks || !head_group) return fail(SVD_ERR_CONFIG, "NULL masks or head_group");
+  auto* P = new svd_plan();
+  P->layout = *layout;
+  int st = make_grid(layout, &P->grid);
+  if (st) {
+    delete P;
+    return st;
+  }
+  const int64_t nb = P->grid.nb;
+  P->n_heads = n_heads;
+  P->groups.resize(n_groups);
+  for (int32_t g = 0; g < n_groups; ++g) {
+    Group& grp = P->groups[g];
+    grp.skip = group_skip && group_skip[g];
+    grp.spec.mode = grp.skip ? SVD_SKIP : SVD_FULL;  // explicit masks carry no spec
+    if (!grp.skip) {
+      grp.active.assign(masks + size_t(g) * nb * nb, masks + size_t(g + 1) * nb * nb);
+      // attention.py:72-73 sparse_attention rejects an empty query row
+      for (int64_t i = 0; i < nb; ++i) {
+        bool any = false;
+        for (int64_t j = 0; j < nb && !any; ++j) any = grp.active[i * nb + j] != 0;
+        if (!any) {
+          delete P;
+          return fail(SVD_ERR_DEGENERATE_ROW, "mask has a query row with no active key blocks");
+        }
+      }
+    }
+  }
+  P->head_group.assign(head_group, head_group + n_heads);
+  for (int32_t h = 0; h < n_heads; ++h) {
+    if (P->head_group[h] < 0 || P->head_group[h] >= n_groups) {
+      delete P;
+      return fail(SVD_ERR_CONFIG, "head_group out of range");
+    }
+    P->groups[P->head_group[h]].heads.push_back(h);
+  }
+  finalize_plan(P);
+  *plan = P;
+  return SVD_OK;
+}
+
+void svd_plan_destroy(svd_plan* plan) {
+  if (!plan) return;
+  release_device_tables(plan);
+  delete plan;
+}
+
+int svd_plan_get_info(const svd_plan* P, svd_plan_info* info) {
+  if (!P || !info) return fail(SVD_ERR_CONFIG, "NULL argument");
+  info->n_tokens = P->grid.n;
+  info->n_blocks = P->grid.nb;
+  info->n_segments = P->nseg;
+  info->n_heads = P->n_heads;
+  info->n_groups = int32_t(P->groups.size());
+  info->fine_mask = P->fine ? 1 : 0;
+  info->sharded = P->sharded ? 1 : 0;
+  info->n_work_items = int64_t(P->items.size());
+  info->n_kv_entries = int64_t(P->kv.size());
+  info->computed_tiles = P->computed_tiles;
+  info->active_pairs = P->active_pairs;
+  info->dense_pairs = double(P->grid.n) * double(P->grid.n) * double(P->n_heads);
+  return SVD_OK;
+}
+
+int svd_plan_group_heads(const svd_plan* P, int32_t g, int32_t* heads, int32_t* n_heads,
+                         int32_t* is_skip) {
+  if (!P || g < 0 || g >= int32_t(P->groups.size())) return fail(SVD_ERR_CONFIG, "bad group index");
+  const Group& grp = P->groups[g];
+  if (n_heads) *n_heads = int32_t(grp.heads.size());
+  if (heads) std::copy(grp.heads.begin(), grp.heads.end(), heads);
+  if (is_skip) *is_skip = grp.skip ? 1 : 0;
+  return SVD_OK;
+}
+
+int svd_plan_group_mask(const svd_plan* P, int32_t g, uint8_t* active) {
+  if (!P || g < 0 || g >= int32_t(P->groups.size())) return fail(SVD_ERR_CONFIG, "bad group index");
+  const Group& grp = P->groups[g];
+  if (grp.skip) return fail(SVD_ERR_CONFIG, "SKIP group has no mask");
+  std::copy(grp.active.begin(), grp.active.end(), active);
+  return SVD_OK;
+}
+
+int svd_plan_group_nnz(const svd_plan* P, int32_t g, int64_t* nnz) {
+  if (!P || g < 0 || g >= int32_t(P->groups.size())) return fail(SVD_ERR_CONFIG, "bad group index");
+  const Group& grp = P->groups[g];
+  int64_t c = 0;
+  for (uint8_t a : grp.active) c += a != 0;
+  *nnz = c;
+  return SVD_OK;
+}
+
+// patterns.py:363-366 active_key_blocks(qb) = flatnonzero(active[qb]), per row
+int svd_plan_group_csr(const svd_plan* P, int32_t g, int64_t* row_ptr, int64_t* col_idx) {
+  if (!P || g < 0 || g >= int32_t(P->groups.size())) return fail(SVD_ERR_CONFIG, "bad group index");
+  const Group& grp = P->groups[g];
+  const int64_t nb = P->grid.nb;
+  row_ptr[0] = 0;
+  int64_t c = 0;
+  for (int64_t i = 0; i < nb; ++i) {
+    if (!grp.skip)
+      for (int64_t j = 0; j < nb; ++j)
+        if (grp.active[i * nb + j]) col_idx[c++] = j;
+    row_ptr[i + 1] = c;
+  }
+  return SVD_OK;
+}
+
+int svd_plan_schedule(const svd_plan* P, int32_t* items, int32_t* kv) {
+  if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
+  if (items) std::memcpy(items, P->items.data(), P->items.size() * sizeof(WorkItem));
+  if (kv) std::memcpy(kv, P->kv.data(), P->kv.size() * sizeof(KvEntry));
+  return SVD_OK;
+}
+
+int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** shard) {
+  if (!P || !shard) return fail(SVD_ERR_CONFIG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SVD_ERR_CONFIG, "bad world/rank");
+  auto* S = new svd_plan();
+  S->layout = P->layout;
+  S->grid = P->grid;
+  S->nseg = P->nseg;
+  S->n_heads = P->n_heads;
+  S->fine = P->fine;
+  S->head_group = P->head_group;
+  S->groups = P->groups;
+  S->kv = P->kv;
+  S->fine_bits = P->fine_bits;
+  S->fine_bit_off = P->fine_bit_off;
+  S->active_pairs = P->active_pairs;
+  S->sharded = true;
+  // LPT over ranks on the tile cost (items are already heaviest-first)
+  std::vector<double> load(world, 0.0);
+  for (const auto& it : P->items) {
+    const double cost = it.kv_count > 0 ? double(it.kv_count) : 0.05;
+    int32_t best = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
+    load[best] += cost;
+    if (best != rank) continue;
+    WorkItem w = it;
+    w.out_base = int32_t(S->n_rows);
+    for (int k = 0; k < kSlotsPerItem; ++k) {
+      if (w.qseg[k] < 0) continue;
+      for (int r = 0; r < kSeg; ++r) {
+        const int64_t tok = int64_t(w.qseg[k]) * kSeg + r;
+        S->row_head.push_back(tok < P->grid.n ? w.head : -1);
+        S->row_token.push_back(tok < P->grid.n ? int32_t(tok) : -1);
+      }
+      S->n_rows += kSeg;
+    }
+    S->items.push_back(w);
+  }
+  S->computed_tiles = 0;
+  for (const auto& it : S->items) S->computed_tiles += 2 * int64_t(it.kv_count);
+  *shard = S;
+  return SVD_OK;
+}
+
+int svd_plan_shard_rows(const svd_plan* S, int64_t* n_rows, int32_t* row_head, int32_t* row_token) {
+  if (!S || !S->sharded) return fail(SVD_ERR_CONFIG, "not a shard plan");
+  if (n_rows) *n_rows = S->n_rows;
+  if (row_head) std::copy(S->row_head.begin(), S->row_head.end(), row_head);
+  if (row_token) std::copy(S->row_token.begin(), S->row_token.end(), row_token);
+  return SVD_OK;
+}
+
+}  // extern "C"
