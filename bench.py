@@ -1,0 +1,440 @@
+"""Benchmark: one vDiT sparse-attention layer (the Sparse-vDiT hot path) on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                [--config hunyuan|cogvideo|wan|synthetic4k] [--sweep]
+
+A step = the whole layer's attention for one batch: every head of the layer,
+FULL / SKIP / diagonal / multi-diagonal / vertical-stripe heads in ONE fused
+kernel launch (plus, for N>1, the NCCL all-gather that reassembles the head
+dimension and the unpack kernel).  Inputs are synthetic bf16 Q/K/V of the
+named layer shape, resident in HBM; the 2+ GB of inputs exceed the 126 MB L2,
+so no L2 flush is needed between steps.
+
+value = effective (dense-equivalent) TFLOP/s = 4*N^2*d*H / t for the whole
+job; ms_per_step = ms per layer.  roofline = active-tile FLOPs (the
+reference's FLOP convention, costmodel.py:26-32) / kernel time vs the measured
+bf16 tensor peak.  e2e = the same layer through the public API with host
+(pinned) Q/K/V copied in and O copied out every step.  cpu_baseline = the
+reference algorithm (oracle port, fp64 NumPy) timed on this host on a bounded
+sample of query blocks, extrapolated by active FLOPs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "vDiT sparse-attn ms/layer & effective TFLOPS at 86k/120k tokens, 1/2/4/8 B200"
+
+# BASELINE.json configs / SURVEY §8(d): layout, heads x head_dim, mode mix F/S/D/MD/VS
+CONFIGS = {
+    "hunyuan": dict(name="HunyuanVideo layer (119,056 tokens, 24x128)", layout=(256, 33, 3600, 64),
+                    heads=24, d=128, mix=(6, 1, 6, 6, 5)),
+    "cogvideo": dict(name="CogVideoX1.5 layer (85,906 tokens, 48x64)", layout=(226, 21, 4080, 64),
+                     heads=48, d=64, mix=(14, 2, 11, 11, 10)),
+    "wan": dict(name="Wan2.1 layer (75,600 tokens, 40x128)", layout=(0, 21, 3600, 64),
+                heads=40, d=128, mix=(17, 2, 7, 7, 7)),
+    "synthetic4k": dict(name="synthetic 4k layer (4,096 tokens, 8x64)", layout=(0, 16, 256, 64),
+                        heads=8, d=64, mix=None),
+}
+
+
+def assignment_for(cfg, S):
+    """Per-head specs for a config: the paper-derived mode mix with distinct
+    stripe columns per stripe head (seeded), in a fixed shuffled head order."""
+    layout = S.TokenLayout(*cfg["layout"])
+    nb = layout.n_blocks
+    if cfg["mix"] is None:  # config 1 table
+        return [S.full_spec(), S.diagonal_spec(1), S.multi_diagonal_spec(),
+                S.vertical_stripe_spec(stripes=(0, 7)), S.skip_spec(), S.diagonal_spec(1),
+                S.multi_diagonal_spec(), S.vertical_stripe_spec(stripes=(3, 40))]
+    f, s, d, md, vs = cfg["mix"]
+    rng = np.random.default_rng(2506_03065)
+    stripes = [tuple(int(c) for c in rng.choice(nb, size=2, replace=False)) for _ in range(vs)]
+    specs = ([S.full_spec()] * f + [S.skip_spec()] * s + [S.diagonal_spec(1)] * d +
+             [S.multi_diagonal_spec()] * md + [S.vertical_stripe_spec(stripes=c) for c in stripes])
+    order = rng.permutation(len(specs))
+    return [specs[i] for i in order]
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        obj = json.loads(p.read_text())
+        return {"bf16": obj.get("bf16_tflops"), "bf16_sustained": obj.get("bf16_tflops_sustained"),
+                "hbm": obj.get("hbm_gbs"), "source": "measured"}
+    return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "source": "fallback"}
+
+
+def ncu_traffic(cfg_key: str):
+    """dram bytes per launch of the fused kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        obj = json.loads(p.read_text())
+        return obj.get(cfg_key, {}).get("dram_bytes_per_launch")
+    except (ValueError, OSError):
+        return None
+
+
+# ----------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_baseline(cfg, S, budget_s: float = 15.0) -> dict:
+    """Time the reference algorithm (fp64 streaming online softmax, the oracle
+    port of attention.py:57-98) on this host over a bounded sample of query
+    blocks of one head per distinct mode at full N, and extrapolate to the
+    whole layer by active FLOPs per mode."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import svdit_oracle as O
+
+    text, frames, tpf, bs = cfg["layout"]
+    og = O.block_grid(text, frames, tpf, bs)
+    n, d = og.n, cfg["d"]
+    specs = assignment_for(cfg, S)
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((1, 1, n, d), dtype=np.float32)
+    k = rng.standard_normal((1, 1, n, d), dtype=np.float32)
+    v = rng.standard_normal((1, 1, n, d), dtype=np.float32)
+    per_mode = {}
+    for spec in specs:
+        per_mode.setdefault(int(spec.mode), spec)
+    modes = [m for m in per_mode if m != 1]
+    slice_s = budget_s / max(1, len(modes))
+    total_flops_layer = 0.0
+    total_time_layer = 0.0
+    sampled = []
+    for m in modes:
+        spec = per_mode[m]
+        active = O.build_mask(spec, og)
+        heads_m = sum(1 for s in specs if int(s.mode) == m)
+        # layer FLOPs of this mode (all its heads; stripe heads differ only in columns)
+        flops_mode = sum(4.0 * d * O.active_pairs(O.build_mask(s, og), og.bounds)
+                         for s in specs if int(s.mode) == m)
+        order = rng.permutation(og.n_blocks)
+        t0 = time.perf_counter()
+        done_flops = 0.0
+        nq = 0
+        for qb in order:
+            O.sparse_attention_rows(q, k, v, active, og.bounds, [int(qb)])
+            rows = og.bounds[qb + 1] - og.bounds[qb]
+            cols = float(np.diff(og.bounds)[active[qb]].sum())
+            done_flops += 4.0 * d * rows * cols
+            nq += 1
+            if time.perf_counter() - t0 > slice_s:
+                break
+        dt = time.perf_counter() - t0
+        rate = done_flops / dt
+        total_flops_layer += flops_mode
+        total_time_layer += flops_mode / rate
+        sampled.append(f"{S.Mode(m).label}:{nq}qb/{heads_m}h "
+                       f"{rate / 1e9:.1f}GF/s")
+    dense = 4.0 * n * n * d * cfg["heads"]
+    return {
+        "value": dense / total_time_layer / 1e12,
+        "unit": "TFLOP/s (dense-equivalent)",
+        "ms_per_layer": total_time_layer * 1e3,
+        "active_gflops_per_s": total_flops_layer / total_time_layer / 1e9,
+        "cores": os.cpu_count(),
+        "kind": "port",
+        "sample": (f"fp64 NumPy oracle (attention.py:57-98 restated), 1 head per mode at full N={n}, "
+                   f"random query blocks for ~{slice_s:.0f}s each [{'; '.join(sampled)}], "
+                   f"extrapolated by active FLOPs; BLAS threads = all {os.cpu_count()} host cores"),
+    }
+
+
+# ----------------------------------------------------------------- GPU arm
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if os.environ.get("SVD_BACKEND", "nccl") == "nccl" else "gloo")
+    return world, rank, local
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2506_03065_b200 as S
+    from paper_2506_03065_b200.sharding import HeadShardedLayer
+
+    world, rank, local = init_dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    layout = S.TokenLayout(*cfg["layout"])
+    n, H, d = layout.total_tokens, cfg["heads"], cfg["d"]
+    specs = assignment_for(cfg, S)
+    plan = S.plan_for_assignment(specs, layout)
+    info = plan.info
+    f_active = plan.active_flops(d)
+    f_dense = plan.dense_flops(d)
+
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    q = torch.randn(1, H, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+    k = torch.randn(1, H, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+    v = torch.randn(1, H, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+    layer = HeadShardedLayer(plan, world, rank, head_dim=d, device=dev)
+    out = torch.empty(1, H, n, d, device=dev, dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        layer(q, k, v, out)
+    barrier()
+    # kernel-only events around each fused launch (same stream) for the roofline
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        barrier()
+        t0.record(stream)
+        for i in range(args.steps):
+            layer(q, k, v, out, kernel_events=kev[i])
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([ms, kms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, kms = float(tt[0]), float(tt[1])
+    clock = clocks.summary()
+
+    # end to end through the public API: pinned host Q/K/V in, O out, every step
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    groups = S.group_heads(specs, S.block_grid(layout))
+    for _ in range(2):
+        layer.e2e(hq, hk, hv, hout, groups)
+    barrier()
+    te = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        layer.e2e(hq, hk, hv, hout, groups)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt[0])
+
+    # dense sm_100a baseline on the same GPU: every head FULL through the same kernel
+    dense_ms = None
+    if not args.no_dense and world == 1:
+        dplan = S.plan_for_assignment([S.full_spec()] * H, layout)
+        dense_out = torch.empty_like(out)
+        for _ in range(2):
+            dplan.forward(q, k, v, dense_out, head_dim=d)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        reps = 3
+        for _ in range(reps):
+            dplan.forward(q, k, v, dense_out, head_dim=d)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        dense_ms = a.elapsed_time(b) / reps
+
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    # the fused kernel launch per rank handles 1/world of the active FLOPs
+    achieved = f_active / world / (kms * 1e-3) / 1e12
+    traffic = ncu_traffic(args.config)
+    line = {
+        "metric": METRIC,
+        "value": round(f_dense / (ms * 1e-3) / 1e12, 2),
+        "unit": "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (torch.randn Q/K/V, seed 1234)",
+        "config": {
+            "workload": cfg["name"],
+            "layout": {"text_tokens": cfg["layout"][0], "frames": cfg["layout"][1],
+                       "tokens_per_frame": cfg["layout"][2], "block_size": cfg["layout"][3]},
+            "heads": H, "head_dim": d, "batch": 1,
+            "mode_mix_F_S_D_MD_VS": cfg["mix"],
+            "density": round(f_active / f_dense, 4),
+            "parallelism": f"head/q-range sharded x{world} + NCCL all-gather" if world > 1 else "1 GPU",
+            "l2": "inputs 3 x %.0f MB bf16 > 126 MB L2: no flush" % (H * n * d * 2 / 1e6),
+        },
+        "ms_per_layer": round(ms, 4),
+        "active_tflops": round(f_active / (ms * 1e-3) / 1e12, 2),
+        "kernel_ms": round(kms, 4),
+        "dense_ms": round(dense_ms, 3) if dense_ms else None,
+        "speedup_vs_dense": round(dense_ms / ms, 3) if dense_ms else None,
+        "roofline": {
+            "bound": "tensor",
+            "achieved": round(achieved, 2),
+            "peak": peaks["bf16_sustained"],
+            "unit": "TFLOP/s",
+            "frac": round(achieved / peaks["bf16_sustained"], 4),
+            "traffic": traffic,
+            "peak_kind": f"{peaks['source']} sustained cuBLAS bf16 (kernel timed inside a long loop)",
+            "frac_of_burst_peak": round(achieved / peaks["bf16"], 4),
+            "algorithmic_flops_per_launch": f_active / world,
+            "issued_tile_flops_per_launch": info.computed_tiles * 4.0 * 128 * 128 * d / world,
+        },
+        "e2e": {
+            "value": round(f_dense / (e2e_ms * 1e-3) / 1e12, 2),
+            "unit": "TFLOP/s (effective, dense-equivalent)",
+            "ms_per_layer": round(e2e_ms, 3),
+            "h2d_bytes_per_step": 3 * H * n * d * 2,
+            "d2h_bytes_per_step": H * n * d * 2,
+            "path": "fused_layer_attention-equivalent public API (LayerPlan) with pinned host bf16 Q/K/V",
+        },
+        "gpu_launches": args.steps * (1 if world == 1 else 2),
+        "clocks": clock,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, S, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (oracle port;
+    /root/reference is not available on the GPU box)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2506_03065_b200 as S
+
+    cfg = CONFIGS[args.config]
+    n = cfg["layout"][0] + cfg["layout"][1] * cfg["layout"][2]
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, S, budget_s=budget)
+    vals = [cpu_baseline(cfg, S, budget_s=budget) for _ in range(args.steps)]
+    value = statistics.median(v["value"] for v in vals)
+    ms = statistics.median(v["ms_per_layer"] for v in vals)
+    cb = dict(vals[0])
+    cb["value"] = value
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)",
+        "impl": "reference", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "tokens": n, "heads": cfg["heads"], "head_dim": cfg["d"]},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="hunyuan")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

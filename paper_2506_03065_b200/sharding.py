@@ -1,0 +1,91 @@
+"""Head / query-range sharding of one layer over the GPUs of a box.
+
+Heads are independent (attention.py:211 writes only out[:, idx]) and so are
+query blocks within a head (attention.py:81-97).  The plan's work items —
+(head, four query segments) with their KV tile lists — are split over ranks
+by LPT on tile cost (svd_plan_shard), so FULL heads are divided by query
+range instead of being indivisible.  Each rank writes its rows into a packed
+buffer; one NCCL all-gather over NVLink reassembles them and the unpack
+kernel scatters the rows back into O[B=1, H, N, d].  Q/K/V are replicated on
+every rank, as layer_qkv produces them (model.py:372-391).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from .attention import LayerPlan
+
+
+class HeadShardedLayer:
+    """Callable running one layer's attention on `world` ranks (1 = plain launch)."""
+
+    def __init__(self, plan: LayerPlan, world: int, rank: int, head_dim: int, device):
+        import torch
+
+        self.plan = plan
+        self.world = world
+        self.rank = rank
+        self.head_dim = head_dim
+        self.device = device
+        self.tensor_dim = 64 if head_dim <= 64 else 128
+        if world == 1:
+            self.shard = None
+            return
+        shards = [plan.shard(world, r) for r in range(world)]
+        rows = [s.shard_rows() for s in shards]
+        self.max_rows = max(1, max(len(h) for h, _ in rows))
+        heads = np.full(world * self.max_rows, -1, dtype=np.int32)
+        toks = np.full(world * self.max_rows, -1, dtype=np.int32)
+        for r, (h, t) in enumerate(rows):
+            heads[r * self.max_rows: r * self.max_rows + len(h)] = h
+            toks[r * self.max_rows: r * self.max_rows + len(t)] = t
+        self.shard = shards[rank]
+        self.row_head = torch.from_numpy(heads).to(device)
+        self.row_token = torch.from_numpy(toks).to(device)
+        self.packed = torch.empty(self.max_rows, self.tensor_dim, dtype=torch.bfloat16, device=device)
+        self.gathered = torch.empty(world * self.max_rows, self.tensor_dim, dtype=torch.bfloat16,
+                                    device=device)
+
+    def __call__(self, q, k, v, out, kernel_events=None):
+        import torch
+
+        stream = torch.cuda.current_stream(self.device)
+        if kernel_events is not None:
+            kernel_events[0].record(stream)
+        if self.shard is None:
+            self.plan.forward(q, k, v, out, head_dim=self.head_dim, stream=stream)
+            if kernel_events is not None:
+                kernel_events[1].record(stream)
+            return out
+        self.shard.forward(q, k, v, self.packed, head_dim=self.head_dim, stream=stream)
+        if kernel_events is not None:
+            kernel_events[1].record(stream)
+        import torch.distributed as dist
+
+        dist.all_gather_into_tensor(self.gathered, self.packed)
+        ost = nat.i64x4(out.stride())
+        nat.check(nat.lib().svd_unpack_rows(
+            nat.c_void_p(self.row_head.data_ptr()), nat.c_void_p(self.row_token.data_ptr()),
+            int(self.world * self.max_rows), nat.c_void_p(self.gathered.data_ptr()),
+            int(self.gathered.stride(0)), nat.c_void_p(out.data_ptr()), ost, int(self.tensor_dim),
+            nat.c_void_p(stream.cuda_stream)))
+        return out
+
+    def e2e(self, hq, hk, hv, hout, groups):
+        """End-to-end step from pinned host buffers: H2D, attention, D2H."""
+        import torch
+
+        from .attention import fused_layer_attention
+
+        q = hq.to(self.device, non_blocking=True)
+        k = hk.to(self.device, non_blocking=True)
+        v = hv.to(self.device, non_blocking=True)
+        if self.shard is None:
+            out = fused_layer_attention(q, k, v, groups)
+        else:
+            out = torch.empty(hout.shape, dtype=torch.bfloat16, device=self.device)
+            self(q, k, v, out)
+        hout.copy_(out, non_blocking=True)
+        return hout
