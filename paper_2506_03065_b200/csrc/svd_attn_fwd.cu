@@ -101,15 +101,17 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* tmap, uint32_t dst,
   }
 }
 
-// Mask one 128-key tile of S for this thread's row.
-__device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, int qslot, int tok_r,
+// Mask one 128-key tile of S for this thread's row.  Segment-grain tiles
+// (block_size % 64 == 0) need only the tile's activity bits and the sequence
+// end; FINE (block_size % 64 != 0) looks up every element's (qb, kb) bit.
+template <bool FINE>
+__device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, int qslot,
                                            const FwdParams& p, const uint32_t* bits_row) {
   const bool on0 = (e.flags >> (2 * qslot)) & 1u;
   const bool on1 = (e.flags >> (2 * qslot + 1)) & 1u;
   const int lim0 = on0 ? min(kSeg, p.n_tokens - e.kseg0 * kSeg) : 0;
   const int lim1 = (on1 && e.kseg1 >= 0) ? min(kSeg, p.n_tokens - e.kseg1 * kSeg) : 0;
-  if (e.flags & kFlagFine) {
-    // block_size % 64 != 0: the (query block, key block) bit of every element
+  if constexpr (FINE) {
 #pragma unroll
     for (int i = 0; i < 128; ++i) {
       const int slot = i >> 6;
@@ -122,17 +124,21 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
       }
       if (!ok) s[i] = -INFINITY;
     }
-    (void)tok_r;
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int i = 0; i < 64; ++i) {
-    if (i >= lim0) s[i] = -INFINITY;
-    if (i >= lim1) s[64 + i] = -INFINITY;
+    for (int i = 0; i < 64; ++i) {
+      if (i >= lim0) s[i] = -INFINITY;
+      if (i >= lim1) s[64 + i] = -INFINITY;
+    }
   }
 }
 
-template <int D>
+// Exp2 offload: of every 8 consecutive column pairs, the last kEmuPairs go
+// through the FMA-pipe polynomial instead of MUFU.ex2 (MUFU is 16/clk/SM and
+// would otherwise co-limit with the tensor pipe).
+constexpr int kEmuPairs = 3;
+
+template <int D, bool FINE>
 __global__ void __launch_bounds__(kThreads, 1)
     svd_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
@@ -175,6 +181,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(base_ptr + C::kOffTmemSlot);
 
+  // Register split: the producer / MMA warpgroup needs few registers, the two
+  // softmax warpgroups hold a 128-wide fp32 row of S each.
+  if (warp < 4) {
+  ptx::reg_dealloc<72>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_kv > 0) {
@@ -278,9 +288,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
 
-  if (warp < 4) return;  // warps 2-3: no role
+  return;  // warps 2-3: no role
+  }  // warp < 4
 
   // -------------------------------------------------------------- softmax / epilogue
+  ptx::reg_alloc<208>();
   const int x = (warp - 4) >> 2;           // Q tile A (0) or B (1)
   const int wq = warp & 3;                 // TMEM lane quarter
   const int row = wq * 32 + lane;          // row of the 128-row tile
@@ -307,15 +319,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   const uint32_t* bits_row = nullptr;
-  if (p.bits != nullptr) {
+  if constexpr (FINE) {
     const int qb = min(max(tok_r, 0) / p.block_size, p.n_blocks - 1);
     bits_row = p.bits + p.bit_off[item.group] + int64_t(qb) * p.words_per_row;
   }
   const float sl2 = p.scale_log2;
+  const float2 sl2x2 = make_float2(sl2, sl2);
   float m = -INFINITY;  // running max (log2 domain); lazily updated
   float l = 0.f;        // running denominator relative to m
+  const KvEntry* kvp = p.kv + item.kv_begin;
+  KvEntry e_next = kvp[0];
 
   for (int j = 0; j < n_kv; ++j) {
+    const KvEntry e = e_next;
+    if (j + 1 < n_kv) e_next = kvp[j + 1];  // prefetch: hidden behind the S wait
     ptx::mbar_wait(bar(C::kBarS + x), j & 1);
     ptx::tc_fence_after();
     float s[128];
@@ -324,13 +341,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
     ptx::tmem_ld32(ts + 64, *reinterpret_cast<float(*)[32]>(&s[64]));
     ptx::tmem_ld32(ts + 96, *reinterpret_cast<float(*)[32]>(&s[96]));
-    const KvEntry e = p.kv[item.kv_begin + j];
     ptx::tmem_wait_ld();
-    if (!(e.flags & kFlagAll)) apply_mask(s, e, qslot, tok_r, p, bits_row);
+    if (!(e.flags & kFlagAll)) apply_mask<FINE>(s, e, qslot, p, bits_row);
 
-    float mx = s[0];
+    // row max: 8 independent FMNMX3 chains, then a short tree
+    float mp[8];
 #pragma unroll
-    for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+    for (int t = 0; t < 8; ++t) mp[t] = fmaxf(s[t], s[8 + t]);
+#pragma unroll
+    for (int i = 16; i < 128; i += 16)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mp[t] = fmaxf(mp[t], fmaxf(s[i + t], s[i + 8 + t]));
+    const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                           fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
     const float m_new = fmaxf(m, mx * sl2);
     // lazy rescale: keep a stale max unless it grew by more than 2^8
     const bool resc = m_new > m + 8.0f;
@@ -354,19 +377,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     const float mref = (m == -INFINITY) ? 0.f : m;
+    const float2 nm = make_float2(-mref, -mref);
     const uint32_t tp = tmem + lane_off + C::col_p(x);
+    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                     make_float2(0.f, 0.f)};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float p0 = ptx::ex2(fmaf(s[c * 32 + 2 * i], sl2, -mref));
-        const float p1 = ptx::ex2(fmaf(s[c * 32 + 2 * i + 1], sl2, -mref));
-        l += p0 + p1;
-        pk[i] = ptx::pack_bf16(p0, p1);
+        const float2 xv = ptx::ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sl2x2, nm);
+        float2 pv;
+        if ((i & 7) >= 8 - kEmuPairs) {
+          pv = ptx::ex2_poly2(xv);
+        } else {
+          pv.x = ptx::ex2(xv.x);
+          pv.y = ptx::ex2(xv.y);
+        }
+        acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
+        pk[i] = ptx::pack_bf16(pv.x, pv.y);
       }
       ptx::tmem_st16(tp + c * 16, pk);
     }
+    const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
+    const float2 a = ptx::fadd2(a01, a23);
+    l += a.x + a.y;
     ptx::tmem_wait_st();
     ptx::tc_fence_before();
     ptx::mbar_arrive(bar(C::kBarP + x));
@@ -518,8 +553,11 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(svd_fwd_kernel<D>,
+    cudaError_t e = cudaFuncSetAttribute(svd_fwd_kernel<D, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(svd_fwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmemBytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     attr_set[dev] = true;
   }
@@ -540,7 +578,10 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   prm.scale_log2 = float(1.4426950408889634 / std::sqrt(double(head_dim)));
   if (T->n_items == 0) return SVD_OK;
   dim3 grid(unsigned(T->n_items), unsigned(batch));
-  svd_fwd_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);
+  if (P->fine)
+    svd_fwd_kernel<D, true><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);
+  else
+    svd_fwd_kernel<D, false><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "svd_fwd_kernel launch");
   return SVD_OK;
