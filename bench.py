@@ -278,6 +278,8 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, kms = float(tt[0]), float(tt[1])
     clock = clocks.summary()
+    if not bool(torch.isfinite(out).all()):
+        raise RuntimeError("non-finite values in the layer output")
 
     # end to end through the public API: pinned host Q/K/V in, O out, every step
     hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
