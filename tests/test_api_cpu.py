@@ -1,0 +1,115 @@
+"""Reference-API behaviour that needs no GPU: argument checks raise the
+reference's exception classes before any device work (attention.py:27-33,
+:66-73, :157-161, :195-199), the strategy-table plugin surface, the cost
+model, and the no-CPU-fallback guarantee."""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2506_03065_b200 as S
+from paper_2506_03065_b200 import _native as nat
+
+
+def qkv(b=1, h=2, n=64, d=8):
+    rng = np.random.default_rng(0)
+    return [rng.standard_normal((b, h, n, d)).astype(np.float32) for _ in range(3)]
+
+
+def test_rank_and_shape_checks():
+    q, k, v = qkv()
+    g = S.block_grid(S.TokenLayout(0, 1, 64, 16))
+    with pytest.raises(S.ShapeError):
+        S.sparse_attention(q[0], k, v, S.build_mask(S.full_spec(), g))
+    with pytest.raises(S.ShapeError):
+        S.fused_layer_attention(q, k[:, :1], v, S.group_heads([S.full_spec()] * 2, g))
+    with pytest.raises(S.ShapeError):
+        S.sparse_attention(q, k, v, S.build_mask(S.full_spec(), S.block_grid(S.TokenLayout(0, 2, 64, 16))))
+
+
+def test_skip_mask_and_empty_row_rejected():
+    q, k, v = qkv()
+    g = S.block_grid(S.TokenLayout(0, 1, 64, 16))
+    with pytest.raises(S.DegenerateRowError):
+        S.sparse_attention(q, k, v, S.build_mask(S.skip_spec(), g))
+    active = np.zeros((4, 4), dtype=bool)
+    active[0, 0] = True
+    with pytest.raises(S.DegenerateRowError):
+        S.sparse_attention(q, k, v, S.BlockMask(grid=g, active=active))
+
+
+def test_groups_must_partition_heads():
+    q, k, v = qkv(h=4, n=32)
+    g = S.block_grid(S.TokenLayout(0, 2, 16, 16))
+    with pytest.raises(S.ConfigError):
+        S.fused_layer_attention(q, k, v, S.group_heads([S.full_spec()] * 3, g))
+    with pytest.raises(S.ConfigError):
+        S.HeadGroup(spec=S.full_spec(), heads=(0, 0), mask=None)
+    with pytest.raises(S.ConfigError):
+        S.HeadGroup(spec=S.full_spec(), heads=(), mask=None)
+
+
+def test_no_cpu_fallback():
+    """Valid arguments on a host without CUDA: the operator raises, it never
+    computes on the CPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    q, k, v = qkv(h=1)
+    g = S.block_grid(S.TokenLayout(0, 1, 64, 64))
+    with pytest.raises(nat.NativeError):
+        S.fused_layer_attention(q, k, v, S.group_heads([S.full_spec()], g))
+    with pytest.raises(nat.NativeError):
+        S.dense_attention(q, k, v)
+
+
+def test_pattern_config_plugin_surface(tmp_path):
+    modes = np.array([[[0, 1, 2, 3, 4]]], dtype=np.uint8)
+    cfg = S.PatternConfig(modes=modes, stripes={(0, 4): (1, 3)})
+    asg = cfg.assignment(0, 0)
+    assert [int(s.mode) for s in asg] == [0, 1, 2, 3, 4]
+    assert asg[4].stripes == (1, 3)
+    path = tmp_path / "cfg.json"
+    cfg.save(path)
+    back = S.PatternConfig.load(path)
+    assert back.to_json() == cfg.to_json()
+    doc = json.loads(path.read_text())
+    assert doc["dims"] == [1, 1, 5]
+    layout = S.TokenLayout(0, 8, 64, 64)
+    groups = S.group_heads(asg, S.block_grid(layout))
+    assert len(groups) == 5
+    s = S.config_sparsity(cfg, layout)
+    assert 0 < s < 1
+
+
+def test_mode_loss_and_select_mode():
+    a = np.zeros((1, 1, 4, 2))
+    b = np.ones((1, 1, 4, 2))
+    assert S.mode_loss(a, b, 0.75, 0.5) == pytest.approx(1.0 + 0.5 * 0.25)
+    assert S.mode_loss(a, b, 0.75, 0.5, "alg1_sparsity") == pytest.approx(1.0 + 0.5 * 0.75)
+    assert S.select_mode([2, 2, 2, 2], [1, 0.5, 0.5, 0.5], 1.0) is S.Mode.FULL
+    assert S.select_mode([0.1, 0.1, 0.2, 0.3], [1.0, 0.6, 0.5, 0.5], 1.0) is S.Mode.SKIP
+    assert S.select_mode([0.3, 0.1, 0.1, 0.3], [1.0, 0.5, 0.6, 0.5], 1.0) is S.Mode.MULTI_DIAGONAL
+    with pytest.raises(S.ConfigError):
+        S.select_mode([1, 2, 3], [0, 0, 0], 1.0)
+
+
+def test_cost_model_conventions():
+    assert S.attention_flops(1024, 64, 1, 0.0) == 268_435_456
+    short = S.attention_latency_share(45_106, 128, 24)
+    long = S.attention_latency_share(119_056, 128, 24)
+    assert 0 < short < long < 1
+    assert round(short, 4) == 0.7099 and round(long, 4) == 0.8659
+    m = S.B200LatencyModel(launch_ms=0.01, ms_per_tile={128: 1e-5})
+    assert m.effective_sparsity(500, 1000, 128) == pytest.approx(1 - (0.01 + 0.005) / (0.01 + 0.01))
+
+
+def test_layer_plan_flops_match_reference_convention():
+    layout = S.TokenLayout(0, 16, 256, 64)
+    asg = [S.full_spec(), S.diagonal_spec(1), S.skip_spec()]
+    plan = S.plan_for_assignment(asg, layout)
+    g = S.block_grid(layout)
+    want = sum(S.attention_flops(4096, 64, 1, S.sparsity(s, g)) for s in asg if s.mode is not S.Mode.SKIP)
+    assert plan.active_flops(64) == pytest.approx(want, rel=1e-12)
