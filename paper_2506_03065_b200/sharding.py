@@ -18,6 +18,21 @@ from . import _native as nat
 from .attention import LayerPlan
 
 
+def gathered_row_maps(plan: LayerPlan, world: int):
+    """(shards, row_head, row_token, max_rows) for the all-gathered buffer:
+    rank r's packed rows occupy [r*max_rows, (r+1)*max_rows); padding rows and
+    rows past the sequence end carry head -1 (skipped by the unpack)."""
+    shards = [plan.shard(world, r) for r in range(world)]
+    rows = [s.shard_rows() for s in shards]
+    max_rows = max(1, max(len(h) for h, _ in rows))
+    heads = np.full(world * max_rows, -1, dtype=np.int32)
+    toks = np.full(world * max_rows, -1, dtype=np.int32)
+    for r, (h, t) in enumerate(rows):
+        heads[r * max_rows: r * max_rows + len(h)] = h
+        toks[r * max_rows: r * max_rows + len(t)] = t
+    return shards, heads, toks, max_rows
+
+
 class HeadShardedLayer:
     """Callable running one layer's attention on `world` ranks (1 = plain launch)."""
 
@@ -33,14 +48,7 @@ class HeadShardedLayer:
         if world == 1:
             self.shard = None
             return
-        shards = [plan.shard(world, r) for r in range(world)]
-        rows = [s.shard_rows() for s in shards]
-        self.max_rows = max(1, max(len(h) for h, _ in rows))
-        heads = np.full(world * self.max_rows, -1, dtype=np.int32)
-        toks = np.full(world * self.max_rows, -1, dtype=np.int32)
-        for r, (h, t) in enumerate(rows):
-            heads[r * self.max_rows: r * self.max_rows + len(h)] = h
-            toks[r * self.max_rows: r * self.max_rows + len(t)] = t
+        shards, heads, toks, self.max_rows = gathered_row_maps(plan, world)
         self.shard = shards[rank]
         self.row_head = torch.from_numpy(heads).to(device)
         self.row_token = torch.from_numpy(toks).to(device)
