@@ -198,3 +198,34 @@ def test_deterministic():
     a = _gpu_fused(lay, specs, q, k, v)
     b = _gpu_fused(lay, specs, q, k, v)
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_packed_rows_and_unpack_on_gpu(world):
+    """The multi-GPU data path on one device: every shard plan writes its
+    packed rows, the gathered buffer is unpacked by svd_unpack_rows, and the
+    result equals the single-launch layer output bit for bit."""
+    import torch
+
+    from paper_2506_03065_b200 import _native as nat
+    from paper_2506_03065_b200.sharding import gathered_row_maps
+
+    lay = (96, 16, 250, 64)
+    specs = [S.full_spec(), S.diagonal_spec(1), S.skip_spec(), S.multi_diagonal_spec(),
+             S.vertical_stripe_spec(stripes=(5, 33))]
+    q, k, v = (_dev(x) for x in _inputs(9, 1, len(specs), 4096, 128, 2.0))
+    plan = S.LayerPlan.from_specs(specs, S.TokenLayout(*lay))
+    ref = torch.empty_like(q)
+    plan.forward(q, k, v, ref, head_dim=128)
+    shards, heads, toks, max_rows = gathered_row_maps(plan, world)
+    gathered = torch.zeros(world * max_rows, 128, dtype=torch.bfloat16, device="cuda")
+    for r, sh in enumerate(shards):
+        sh.forward(q, k, v, gathered[r * max_rows:(r + 1) * max_rows], head_dim=128)
+    out = torch.full_like(q, float("nan"))
+    rh, rt = torch.from_numpy(heads).cuda(), torch.from_numpy(toks).cuda()
+    nat.check(nat.lib().svd_unpack_rows(
+        nat.c_void_p(rh.data_ptr()), nat.c_void_p(rt.data_ptr()), int(world * max_rows),
+        nat.c_void_p(gathered.data_ptr()), int(gathered.stride(0)), nat.c_void_p(out.data_ptr()),
+        nat.i64x4(out.stride()), 128, nat.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
