@@ -44,23 +44,30 @@ struct KCfg {
   static constexpr int kTileBytes = 128 * D * 2;       // a Q tile or a KV tile
   static constexpr int kKSt = D == 128 ? 2 : 4;
   static constexpr int kVSt = D == 128 ? 2 : 4;
+  // d=64 leaves TMEM room for P next to S: S_X(j+1) is then issued as soon as
+  // the softmax has read S_X(j) ("early S"), decoupling the two pipelines.
+  // d=128 needs all 512 columns for S_A, S_B, O_A, O_B, so P_X aliases S_X and
+  // S_X(j+1) must follow PV_X(j).
+  static constexpr bool kEarlyS = D == 64;
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + 2 * kTileBytes;
   static constexpr int kOffV = kOffK + kKSt * kTileBytes;
   static constexpr int kOffBar = kOffV + kVSt * kTileBytes;
-  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p[2] o[2]
+  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p0[2] p1[2] o[2] sfree[2] pvdone[2]
   static constexpr int kBarQ = 0;
   static constexpr int kBarKF = 1;
   static constexpr int kBarKE = kBarKF + kKSt;
   static constexpr int kBarVF = kBarKE + kKSt;
   static constexpr int kBarVE = kBarVF + kVSt;
   static constexpr int kBarS = kBarVE + kVSt;
-  static constexpr int kBarP = kBarS + 2;
-  static constexpr int kBarO = kBarP + 2;
-  static constexpr int kNumBars = kBarO + 2;
+  static constexpr int kBarP0 = kBarS + 2;
+  static constexpr int kBarP1 = kBarP0 + 2;
+  static constexpr int kBarO = kBarP1 + 2;
+  static constexpr int kBarSFree = kBarO + 2;
+  static constexpr int kBarPVDone = kBarSFree + 2;
+  static constexpr int kNumBars = kBarPVDone + 2;
   static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
-  // TMEM columns.  d=128 uses all 512: P_X aliases the first 64 columns of S_X.
   __device__ static constexpr uint32_t col_s(int x) { return x ? 128u : 0u; }
   __device__ static constexpr uint32_t col_o(int x) { return x ? 256u + D : 256u; }
   __device__ static constexpr uint32_t col_p(int x) {
@@ -85,6 +92,16 @@ struct FwdParams {
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ KvEntry load_kv(const KvEntry* ptr) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(ptr));
+  KvEntry e;
+  e.kseg0 = v.x;
+  e.kseg1 = v.y;
+  e.flags = uint32_t(v.z);
+  e.pad = v.w;
+  return e;
 }
 
 template <int D>
@@ -136,7 +153,10 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
 // Exp2 offload: of every 8 consecutive column pairs, the last kEmuPairs go
 // through the FMA-pipe polynomial instead of MUFU.ex2 (MUFU is 16/clk/SM and
 // would otherwise co-limit with the tensor pipe).
-constexpr int kEmuPairs = 3;
+#ifndef SVD_EMU_PAIRS
+#define SVD_EMU_PAIRS 3
+#endif
+constexpr int kEmuPairs = SVD_EMU_PAIRS;
 
 template <int D, bool FINE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -151,9 +171,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   auto bar = [&](int i) { return base + C::kOffBar + 8u * uint32_t(i); };
 
-  const WorkItem item = p.items[blockIdx.x];
+  const WorkItem* itp = p.items + blockIdx.x;
   const int b = blockIdx.y;
-  const int n_kv = item.kv_count;
+  const int n_kv = itp->kv_count;
+  const int head = itp->head;
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(bar(C::kBarQ), 1);
@@ -167,8 +188,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(bar(C::kBarS + x), 1);
-      ptx::mbar_init(bar(C::kBarP + x), 128);
+      ptx::mbar_init(bar(C::kBarP0 + x), 128);
+      ptx::mbar_init(bar(C::kBarP1 + x), 128);
       ptx::mbar_init(bar(C::kBarO + x), 1);
+      ptx::mbar_init(bar(C::kBarSFree + x), 128);
+      ptx::mbar_init(bar(C::kBarPVDone + x), 1);
     }
     ptx::fence_barrier_init();
   }
@@ -184,128 +208,158 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Register split: the producer / MMA warpgroup needs few registers, the two
   // softmax warpgroups hold a 128-wide fp32 row of S each.
   if (warp < 4) {
-  ptx::reg_dealloc<72>();
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && n_kv > 0) {
-      ptx::prefetch_tmap(&tm_q);
-      ptx::prefetch_tmap(&tm_k);
-      ptx::prefetch_tmap(&tm_v);
-      const uint64_t pol_q = ptx::policy_evict_first();
-      const uint64_t pol_kv = ptx::policy_evict_last();
-      int first = item.qseg[0];
-      ptx::mbar_arrive_expect_tx(bar(C::kBarQ), 2 * C::kTileBytes);
+    ptx::reg_dealloc<56>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- TMA producer
+      if (lane == 0 && n_kv > 0) {
+        ptx::prefetch_tmap(&tm_q);
+        ptx::prefetch_tmap(&tm_k);
+        ptx::prefetch_tmap(&tm_v);
+        const uint64_t pol_q = ptx::policy_evict_first();
+        const uint64_t pol_kv = ptx::policy_evict_last();
+        const int first = itp->qseg[0];
+        ptx::mbar_arrive_expect_tx(bar(C::kBarQ), 2 * C::kTileBytes);
 #pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        int s0 = item.qseg[2 * x], s1 = item.qseg[2 * x + 1];
-        s0 = s0 >= 0 ? s0 : first;
-        s1 = s1 >= 0 ? s1 : first;
-        load_tile<D>(&tm_q, base + C::kOffQ + x * C::kTileBytes, bar(C::kBarQ), s0, s1, item.head,
-                     b, pol_q);
-      }
-      for (int j = 0; j < n_kv; ++j) {
-        const KvEntry e = p.kv[item.kv_begin + j];
-        const int k0 = e.kseg0, k1 = e.kseg1 >= 0 ? e.kseg1 : e.kseg0;
-        const int ks = j % C::kKSt, vs = j % C::kVSt;
-        ptx::mbar_wait(bar(C::kBarKE + ks), ((j / C::kKSt) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(bar(C::kBarKF + ks), C::kTileBytes);
-        load_tile<D>(&tm_k, base + C::kOffK + ks * C::kTileBytes, bar(C::kBarKF + ks), k0, k1,
-                     item.head, b, pol_kv);
-        ptx::mbar_wait(bar(C::kBarVE + vs), ((j / C::kVSt) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(bar(C::kBarVF + vs), C::kTileBytes);
-        load_tile<D>(&tm_v, base + C::kOffV + vs * C::kTileBytes, bar(C::kBarVF + vs), k0, k1,
-                     item.head, b, pol_kv);
-      }
-    }
-    __syncwarp();
-    return;
-  }
-
-  if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n_kv > 0) {
-      constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false);
-      constexpr uint32_t id_pv = ptx::idesc_bf16(128, D, true);
-      auto issue_s = [&](int x, int ks) {
-        const uint32_t qb = base + C::kOffQ + x * C::kTileBytes;
-        const uint32_t kb = base + C::kOffK + ks * C::kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
-          ptx::mma_ss(tmem + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
-                      ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
+        for (int x = 0; x < 2; ++x) {
+          int s0 = itp->qseg[2 * x], s1 = itp->qseg[2 * x + 1];
+          s0 = s0 >= 0 ? s0 : first;
+          s1 = s1 >= 0 ? s1 : first;
+          load_tile<D>(&tm_q, base + C::kOffQ + x * C::kTileBytes, bar(C::kBarQ), s0, s1, head, b,
+                       pol_q);
         }
-      };
-      auto issue_pv = [&](int x, int vs, bool acc) {
-        const uint32_t vb = base + C::kOffV + vs * C::kTileBytes;
+        const KvEntry* kvp = p.kv + itp->kv_begin;
+        for (int j = 0; j < n_kv; ++j) {
+          const KvEntry e = load_kv(kvp + j);
+          const int k0 = e.kseg0, k1 = e.kseg1 >= 0 ? e.kseg1 : e.kseg0;
+          const int ks = j % C::kKSt, vs = j % C::kVSt;
+          ptx::mbar_wait(bar(C::kBarKE + ks), ((j / C::kKSt) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(bar(C::kBarKF + ks), C::kTileBytes);
+          load_tile<D>(&tm_k, base + C::kOffK + ks * C::kTileBytes, bar(C::kBarKF + ks), k0, k1,
+                       head, b, pol_kv);
+          ptx::mbar_wait(bar(C::kBarVE + vs), ((j / C::kVSt) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(bar(C::kBarVF + vs), C::kTileBytes);
+          load_tile<D>(&tm_v, base + C::kOffV + vs * C::kTileBytes, bar(C::kBarVF + vs), k0, k1,
+                       head, b, pol_kv);
+        }
+      }
+      __syncwarp();
+      return;
+    }
+    if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer
+      if (lane == 0 && n_kv > 0) {
+        constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false);
+        constexpr uint32_t id_pv = ptx::idesc_bf16(128, D, true);
+        auto issue_s = [&](int x, int ks) {
+          const uint32_t qb = base + C::kOffQ + x * C::kTileBytes;
+          const uint32_t kb = base + C::kOffK + ks * C::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ts(tmem + C::col_o(x), tmem + C::col_p(x) + kk * 8,
-                      ptx::sw128_desc(vb + kk * 2048, C::kSlabBytes, 1024), id_pv,
-                      (acc || kk > 0) ? 1u : 0u);
-      };
-      ptx::mbar_wait(bar(C::kBarQ), 0);
-      ptx::mbar_wait(bar(C::kBarKF + 0), 0);
-      ptx::tc_fence_after();
-      issue_s(0, 0);
-      ptx::mma_commit(bar(C::kBarS + 0));
-      issue_s(1, 0);
-      ptx::mma_commit(bar(C::kBarS + 1));
-      ptx::mma_commit(bar(C::kBarKE + 0));
-      for (int j = 0; j < n_kv; ++j) {
-        const int vs = j % C::kVSt;
-        const int ks1 = (j + 1) % C::kKSt;
-        const bool more = j + 1 < n_kv;
-        ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
-        // tile A
-        ptx::mbar_wait(bar(C::kBarP + 0), j & 1);
-        ptx::tc_fence_after();
-        issue_pv(0, vs, j > 0);
-        if (!more) ptx::mma_commit(bar(C::kBarO + 0));
-        if (more) {
-          ptx::mbar_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
+            ptx::mma_ss(tmem + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
+                        ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
+          }
+        };
+        // O_X += P_X V_j, keys [64*half, 64*half + 64): four K=16 steps
+        auto issue_pv_half = [&](int x, int vs, int half, bool acc) {
+          const uint32_t vb = base + C::kOffV + vs * C::kTileBytes;
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = half * 4 + k4;
+            ptx::mma_ts(tmem + C::col_o(x), tmem + C::col_p(x) + kk * 8,
+                        ptx::sw128_desc(vb + kk * 2048, C::kSlabBytes, 1024), id_pv,
+                        (acc || kk > 0) ? 1u : 0u);
+          }
+        };
+        auto issue_pv = [&](int x, int vs, int j) {
+          ptx::mbar_wait(bar(C::kBarP0 + x), j & 1);
           ptx::tc_fence_after();
-          issue_s(0, ks1);
-          ptx::mma_commit(bar(C::kBarS + 0));
-        }
-        // tile B
-        ptx::mbar_wait(bar(C::kBarP + 1), j & 1);
+          issue_pv_half(x, vs, 0, j > 0);
+          ptx::mbar_wait(bar(C::kBarP1 + x), j & 1);
+          ptx::tc_fence_after();
+          issue_pv_half(x, vs, 1, j > 0);
+        };
+        ptx::mbar_wait(bar(C::kBarQ), 0);
+        ptx::mbar_wait(bar(C::kBarKF + 0), 0);
         ptx::tc_fence_after();
-        issue_pv(1, vs, j > 0);
-        ptx::mma_commit(bar(C::kBarVE + vs));
-        if (!more) ptx::mma_commit(bar(C::kBarO + 1));
-        if (more) {
-          issue_s(1, ks1);
-          ptx::mma_commit(bar(C::kBarS + 1));
-          ptx::mma_commit(bar(C::kBarKE + ks1));
+        issue_s(0, 0);
+        ptx::mma_commit(bar(C::kBarS + 0));
+        issue_s(1, 0);
+        ptx::mma_commit(bar(C::kBarS + 1));
+        ptx::mma_commit(bar(C::kBarKE + 0));
+        for (int j = 0; j < n_kv; ++j) {
+          const int vs = j % C::kVSt;
+          const int ks1 = (j + 1) % C::kKSt;
+          const bool more = j + 1 < n_kv;
+          if constexpr (C::kEarlyS) {
+            // next S tiles as soon as both the softmax has drained S and K_{j+1} landed
+            if (more) {
+              ptx::mbar_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1);
+              ptx::mbar_wait(bar(C::kBarSFree + 0), j & 1);
+              ptx::tc_fence_after();
+              issue_s(0, ks1);
+              ptx::mma_commit(bar(C::kBarS + 0));
+              ptx::mbar_wait(bar(C::kBarSFree + 1), j & 1);
+              ptx::tc_fence_after();
+              issue_s(1, ks1);
+              ptx::mma_commit(bar(C::kBarS + 1));
+              ptx::mma_commit(bar(C::kBarKE + ks1));
+            }
+            ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
+            issue_pv(0, vs, j);
+            ptx::mma_commit(bar(C::kBarPVDone + 0));
+            if (!more) ptx::mma_commit(bar(C::kBarO + 0));
+            issue_pv(1, vs, j);
+            ptx::mma_commit(bar(C::kBarPVDone + 1));
+            ptx::mma_commit(bar(C::kBarVE + vs));
+            if (!more) ptx::mma_commit(bar(C::kBarO + 1));
+          } else {
+            ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
+            // tile A: PV (in two halves, as P arrives), then the next S
+            issue_pv(0, vs, j);
+            if (!more) ptx::mma_commit(bar(C::kBarO + 0));
+            if (more) {
+              ptx::mbar_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1);
+              ptx::tc_fence_after();
+              issue_s(0, ks1);
+              ptx::mma_commit(bar(C::kBarS + 0));
+            }
+            // tile B
+            issue_pv(1, vs, j);
+            ptx::mma_commit(bar(C::kBarVE + vs));
+            if (!more) ptx::mma_commit(bar(C::kBarO + 1));
+            if (more) {
+              issue_s(1, ks1);
+              ptx::mma_commit(bar(C::kBarS + 1));
+              ptx::mma_commit(bar(C::kBarKE + ks1));
+            }
+          }
         }
       }
+      __syncwarp();
+      named_bar_sync(1, 32 + 256);
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc(tmem, kTmemCols);
+      return;
     }
-    __syncwarp();
-    named_bar_sync(1, 32 + 256);
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTmemCols);
-    return;
-  }
-
-  return;  // warps 2-3: no role
+    return;  // warps 2-3: no role
   }  // warp < 4
 
   // -------------------------------------------------------------- softmax / epilogue
-  ptx::reg_alloc<208>();
+  ptx::reg_alloc<224>();
   const int x = (warp - 4) >> 2;           // Q tile A (0) or B (1)
   const int wq = warp & 3;                 // TMEM lane quarter
   const int row = wq * 32 + lane;          // row of the 128-row tile
   const uint32_t lane_off = uint32_t(wq * 32) << 16;
   const int qslot = 2 * x + (row >> 6);
-  const int qseg = item.qseg[qslot];
+  const int qseg = itp->qseg[2 * x + (row >> 6)];
   const int tok_r = qseg * kSeg + (row & 63);
   const bool row_valid = qseg >= 0 && tok_r < p.n_tokens;
   __nv_bfloat16* orow;
   if (p.packed)
-    orow = p.o + (int64_t(item.out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
+    orow = p.o + (int64_t(itp->out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
   else
-    orow = p.o + int64_t(b) * p.o_sb + int64_t(item.head) * p.o_sh + int64_t(tok_r) * p.o_sn;
+    orow = p.o + int64_t(b) * p.o_sb + int64_t(head) * p.o_sh + int64_t(tok_r) * p.o_sn;
 
   if (n_kv == 0) {
     // SKIP head (attention.py:51-54): exact zeros, no scores, no softmax
@@ -321,18 +375,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t* bits_row = nullptr;
   if constexpr (FINE) {
     const int qb = min(max(tok_r, 0) / p.block_size, p.n_blocks - 1);
-    bits_row = p.bits + p.bit_off[item.group] + int64_t(qb) * p.words_per_row;
+    bits_row = p.bits + p.bit_off[itp->group] + int64_t(qb) * p.words_per_row;
   }
   const float sl2 = p.scale_log2;
   const float2 sl2x2 = make_float2(sl2, sl2);
   float m = -INFINITY;  // running max (log2 domain); lazily updated
   float l = 0.f;        // running denominator relative to m
-  const KvEntry* kvp = p.kv + item.kv_begin;
-  KvEntry e_next = kvp[0];
+  const KvEntry* kvp = p.kv + itp->kv_begin;
+  KvEntry e_next = load_kv(kvp);
 
   for (int j = 0; j < n_kv; ++j) {
     const KvEntry e = e_next;
-    if (j + 1 < n_kv) e_next = kvp[j + 1];  // prefetch: hidden behind the S wait
+    if (j + 1 < n_kv) e_next = load_kv(kvp + j + 1);  // prefetch behind the S wait
     ptx::mbar_wait(bar(C::kBarS + x), j & 1);
     ptx::tc_fence_after();
     float s[128];
@@ -342,9 +396,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tmem_ld32(ts + 64, *reinterpret_cast<float(*)[32]>(&s[64]));
     ptx::tmem_ld32(ts + 96, *reinterpret_cast<float(*)[32]>(&s[96]));
     ptx::tmem_wait_ld();
+    if constexpr (C::kEarlyS) {
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(bar(C::kBarSFree + x));  // S_X may now be overwritten by S_X(j+1)
+    }
     if (!(e.flags & kFlagAll)) apply_mask<FINE>(s, e, qslot, p, bits_row);
 
-    // row max: 8 independent FMNMX3 chains, then a short tree
+    // row max: 8 independent FMNMX chains, then a short tree
     float mp[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) mp[t] = fmaxf(s[t], s[8 + t]);
@@ -355,6 +413,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                            fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
     const float m_new = fmaxf(m, mx * sl2);
+    if constexpr (C::kEarlyS) {
+      // O_X and the P_X buffer are still in use by PV_X(j-1) until it completes
+      if (j > 0) {
+        ptx::mbar_wait(bar(C::kBarPVDone + x), (j - 1) & 1);
+        ptx::tc_fence_after();
+      }
+    }
     // lazy rescale: keep a stale max unless it grew by more than 2^8
     const bool resc = m_new > m + 8.0f;
     if (__any_sync(0xffffffffu, resc)) {
@@ -398,13 +463,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[i] = ptx::pack_bf16(pv.x, pv.y);
       }
       ptx::tmem_st16(tp + c * 16, pk);
+      if (c == 1 || c == 3) {
+        // hand P over in two 64-key halves: PV on the first half overlaps
+        // the exps of the second
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar((c == 1 ? C::kBarP0 : C::kBarP1) + x));
+      }
     }
     const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
     const float2 a = ptx::fadd2(a01, a23);
     l += a.x + a.y;
-    ptx::tmem_wait_st();
-    ptx::tc_fence_before();
-    ptx::mbar_arrive(bar(C::kBarP + x));
   }
 
   // epilogue: O / l -> bf16 rows

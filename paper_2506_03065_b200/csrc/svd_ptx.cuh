@@ -193,9 +193,9 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 magic = make_float2(12582912.0f, 12582912.0f);
   const float2 nmagic = make_float2(-12582912.0f, -12582912.0f);
   const float2 mone = make_float2(-1.0f, -1.0f);
-  // p in [0.7, 1.42] has biased exponent 126/127: j >= -125 keeps the sum a
-  // normal number; below that (incl. masked -inf) the result is exactly 0
-  const bool zx = x.x < -125.0f, zy = x.y < -125.0f;
+  // p in [0.7, 1.42] has biased exponent 126/127: clamping j >= -125 keeps
+  // the result a normal number (masked -inf scores give ~2^-125, i.e. 0 to
+  // every bf16 / fp32 sum they enter)
   x.x = fmaxf(x.x, -125.0f);
   x.y = fmaxf(x.y, -125.0f);
   const float2 t = fadd2(x, magic);
@@ -206,8 +206,9 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   p = ffma2(p, f, make_float2(0.6932609677f, 0.6932609677f));
   p = ffma2(p, f, make_float2(0.9999280572f, 0.9999280572f));
   float2 r;
-  r.x = zx ? 0.0f : __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23));
-  r.y = zy ? 0.0f : __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23));
+  // exponent insert as one IMAD: bits(t) * 2^23 == j << 23 (mod 2^32)
+  r.x = __int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x));
+  r.y = __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y));
   return r;
 }
 template <int N>
