@@ -7,6 +7,7 @@ missing or fails to load, every call raises immediately.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_void_p
 from pathlib import Path
 
@@ -20,7 +21,7 @@ from .errors import (
     SvditError,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "libsvdit_b200.so"
+LIB_PATH = Path(os.environ.get("SVD_LIB", Path(__file__).resolve().parent / "libsvdit_b200.so"))
 
 SVD_OK = 0
 _STATUS_TO_EXC = {

@@ -36,6 +36,13 @@ namespace svd {
 constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
 
+#ifndef SVD_EARLY_S
+#define SVD_EARLY_S 0
+#endif
+#ifndef SVD_SPLIT_P
+#define SVD_SPLIT_P 1
+#endif
+
 template <int D>
 struct KCfg {
   static constexpr int kSlabs = D / 64;
@@ -48,7 +55,7 @@ struct KCfg {
   // the softmax has read S_X(j) ("early S"), decoupling the two pipelines.
   // d=128 needs all 512 columns for S_A, S_B, O_A, O_B, so P_X aliases S_X and
   // S_X(j+1) must follow PV_X(j).
-  static constexpr bool kEarlyS = D == 64;
+  static constexpr bool kEarlyS = D == 64 && SVD_EARLY_S;
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + 2 * kTileBytes;
   static constexpr int kOffV = kOffK + kKSt * kTileBytes;
@@ -153,10 +160,14 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
 // Exp2 offload: of every 8 consecutive column pairs, the last kEmuPairs go
 // through the FMA-pipe polynomial instead of MUFU.ex2 (MUFU is 16/clk/SM and
 // would otherwise co-limit with the tensor pipe).
-#ifndef SVD_EMU_PAIRS
-#define SVD_EMU_PAIRS 3
+#ifndef SVD_EMU128
+#define SVD_EMU128 0
 #endif
-constexpr int kEmuPairs = SVD_EMU_PAIRS;
+#ifndef SVD_EMU64
+#define SVD_EMU64 0
+#endif
+template <int D>
+constexpr int kEmuPairs = D == 128 ? SVD_EMU128 : SVD_EMU64;
 
 template <int D, bool FINE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < 16; ++i) {
         const float2 xv = ptx::ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sl2x2, nm);
         float2 pv;
-        if ((i & 7) >= 8 - kEmuPairs) {
+        if ((i & 7) >= 8 - kEmuPairs<D>) {
           pv = ptx::ex2_poly2(xv);
         } else {
           pv.x = ptx::ex2(xv.x);
@@ -463,12 +474,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[i] = ptx::pack_bf16(pv.x, pv.y);
       }
       ptx::tmem_st16(tp + c * 16, pk);
-      if (c == 1 || c == 3) {
+      if ((c == 1 && SVD_SPLIT_P) || c == 3) {
         // hand P over in two 64-key halves: PV on the first half overlaps
         // the exps of the second
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(bar((c == 1 ? C::kBarP0 : C::kBarP1) + x));
+        if (c == 1) ptx::mbar_arrive(bar(C::kBarP0 + x));
+        if (c == 3) {
+          if (!SVD_SPLIT_P) ptx::mbar_arrive(bar(C::kBarP0 + x));
+          ptx::mbar_arrive(bar(C::kBarP1 + x));
+        }
       }
     }
     const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
