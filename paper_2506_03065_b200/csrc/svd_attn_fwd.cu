@@ -42,6 +42,12 @@ constexpr uint32_t kTmemCols = 512;
 #ifndef SVD_SPLIT_P
 #define SVD_SPLIT_P 1
 #endif
+#ifndef SVD_SPLIT_S
+#define SVD_SPLIT_S 0
+#endif
+#ifndef SVD_PINGPONG
+#define SVD_PINGPONG 0
+#endif
 
 template <int D>
 struct KCfg {
@@ -169,6 +175,23 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
 template <int D>
 constexpr int kEmuPairs = D == 128 ? SVD_EMU128 : SVD_EMU64;
 
+#ifdef SVD_TRACE
+// Debug-only pipeline trace: (clock, step<<8 | event) pairs for the first 8
+// CTAs of batch 0; streams 0/1 = softmax tile A/B (warp 4/8, lane 0), 2 = MMA.
+constexpr int kTraceCtas = 8, kTraceEvents = 2048;
+__device__ uint32_t g_trace[kTraceCtas][4][kTraceEvents][2];
+__device__ __forceinline__ void trace_ev(int stream, int& n, int step, int code) {
+  if (blockIdx.x < kTraceCtas && blockIdx.y == 0 && n < kTraceEvents) {
+    g_trace[blockIdx.x][stream][n][0] = uint32_t(clock());
+    g_trace[blockIdx.x][stream][n][1] = uint32_t(step << 8 | code);
+    ++n;
+  }
+}
+#define TRACE(stream, n, step, code) trace_ev(stream, n, step, code)
+#else
+#define TRACE(stream, n, step, code) ((void)0)
+#endif
+
 template <int D, bool FINE>
 __global__ void __launch_bounds__(kThreads, 1)
     svd_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -239,11 +262,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                        pol_q);
         }
         const KvEntry* kvp = p.kv + itp->kv_begin;
+#ifdef SVD_TRACE
+        int ptn = 0;
+#endif
         for (int j = 0; j < n_kv; ++j) {
           const KvEntry e = load_kv(kvp + j);
           const int k0 = e.kseg0, k1 = e.kseg1 >= 0 ? e.kseg1 : e.kseg0;
           const int ks = j % C::kKSt, vs = j % C::kVSt;
           ptx::mbar_wait(bar(C::kBarKE + ks), ((j / C::kKSt) & 1) ^ 1);
+#ifdef SVD_TRACE
+          TRACE(3, ptn, j, 70);
+#endif
           ptx::mbar_arrive_expect_tx(bar(C::kBarKF + ks), C::kTileBytes);
           load_tile<D>(&tm_k, base + C::kOffK + ks * C::kTileBytes, bar(C::kBarKF + ks), k0, k1,
                        head, b, pol_kv);
@@ -264,12 +293,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_s = [&](int x, int ks) {
           const uint32_t qb = base + C::kOffQ + x * C::kTileBytes;
           const uint32_t kb = base + C::kOffK + ks * C::kTileBytes;
+#if SVD_SPLIT_S
+          constexpr uint32_t id_s64 = ptx::idesc_bf16(128, 64, false);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
+              ptx::mma_ss(tmem + C::col_s(x) + hh * 64, ptx::sw128_desc(qb + off, 16, 1024),
+                          ptx::sw128_desc(kb + off + hh * 8192, 16, 1024), id_s64, kk > 0);
+            }
+#else
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
             ptx::mma_ss(tmem + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
                         ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
           }
+#endif
         };
         // O_X += P_X V_j, keys [64*half, 64*half + 64): four K=16 steps
         auto issue_pv_half = [&](int x, int vs, int half, bool acc) {
@@ -282,13 +323,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         (acc || kk > 0) ? 1u : 0u);
           }
         };
+        int tn = 0;
+        (void)tn;
         auto issue_pv = [&](int x, int vs, int j) {
+          TRACE(2, tn, j, 30 + x);
           ptx::mbar_wait(bar(C::kBarP0 + x), j & 1);
+          TRACE(2, tn, j, 40 + x);
           ptx::tc_fence_after();
           issue_pv_half(x, vs, 0, j > 0);
           ptx::mbar_wait(bar(C::kBarP1 + x), j & 1);
+          TRACE(2, tn, j, 50 + x);
           ptx::tc_fence_after();
           issue_pv_half(x, vs, 1, j > 0);
+          TRACE(2, tn, j, 10 + x);
         };
         ptx::mbar_wait(bar(C::kBarQ), 0);
         ptx::mbar_wait(bar(C::kBarKF + 0), 0);
@@ -331,9 +378,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!more) ptx::mma_commit(bar(C::kBarO + 0));
             if (more) {
               ptx::mbar_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1);
+              TRACE(2, tn, j + 1, 60);
               ptx::tc_fence_after();
               issue_s(0, ks1);
+              TRACE(2, tn, j + 1, 61);
               ptx::mma_commit(bar(C::kBarS + 0));
+              TRACE(2, tn, j + 1, 20);
             }
             // tile B
             issue_pv(1, vs, j);
@@ -343,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               issue_s(1, ks1);
               ptx::mma_commit(bar(C::kBarS + 1));
               ptx::mma_commit(bar(C::kBarKE + ks1));
+              TRACE(2, tn, j + 1, 21);
             }
           }
         }
@@ -395,10 +446,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const KvEntry* kvp = p.kv + itp->kv_begin;
   KvEntry e_next = load_kv(kvp);
 
+#ifdef SVD_TRACE
+  int tn = 0;
+  const bool tr = (warp == 4 || warp == 8) && lane == 0;
+#endif
+  // Ping-pong: the two tiles' softmax warpgroups take turns on the exp phase
+  // (named barriers 2 = A's turn, 3 = B's turn), so one tile's MUFU work
+  // overlaps the other tile's MMAs instead of both contending for MUFU.
+  if (SVD_PINGPONG && x == 1) asm volatile("bar.arrive 2, 256;" ::: "memory");
   for (int j = 0; j < n_kv; ++j) {
     const KvEntry e = e_next;
     if (j + 1 < n_kv) e_next = load_kv(kvp + j + 1);  // prefetch behind the S wait
+#ifdef SVD_TRACE
+    if (tr) TRACE(x, tn, j, 0);
+#endif
     ptx::mbar_wait(bar(C::kBarS + x), j & 1);
+#ifdef SVD_TRACE
+    if (tr) TRACE(x, tn, j, 1);
+#endif
     ptx::tc_fence_after();
     float s[128];
     const uint32_t ts = tmem + lane_off + C::col_s(x);
@@ -455,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float mref = (m == -INFINITY) ? 0.f : m;
     const float2 nm = make_float2(-mref, -mref);
     const uint32_t tp = tmem + lane_off + C::col_p(x);
+    if (SVD_PINGPONG) named_bar_sync(2 + x, 256);  // wait for my turn
     float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                      make_float2(0.f, 0.f)};
 #pragma unroll
@@ -483,6 +549,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c == 3) {
           if (!SVD_SPLIT_P) ptx::mbar_arrive(bar(C::kBarP0 + x));
           ptx::mbar_arrive(bar(C::kBarP1 + x));
+          // hand the turn to the other tile (B skips its very last hand-over)
+          if (SVD_PINGPONG && (x == 0 || j + 1 < n_kv)) {
+            if (x == 0) asm volatile("bar.arrive 3, 256;" ::: "memory");
+            else asm volatile("bar.arrive 2, 256;" ::: "memory");
+          }
+#ifdef SVD_TRACE
+          if (tr) TRACE(x, tn, j, 2);
+#endif
         }
       }
     }
@@ -709,6 +783,20 @@ int svd_attn_fwd(const svd_plan* P, const void* q, const void* k, const void* v,
                   "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
   }
 }
+
+#ifdef SVD_TRACE
+int svd_debug_trace(void* host, int64_t bytes, int32_t reset) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && host) e = cudaMemcpyFromSymbol(host, g_trace, size_t(bytes));
+  if (e == cudaSuccess && reset) {
+    void* ptr = nullptr;
+    e = cudaGetSymbolAddress(&ptr, g_trace);
+    if (e == cudaSuccess) e = cudaMemset(ptr, 0, sizeof(g_trace));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  return e == cudaSuccess ? SVD_OK : cuda_fail(e, "trace");
+}
+#endif
 
 int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, int64_t n_rows,
                     const void* packed, int64_t packed_row_stride, void* o, const int64_t* o_strides,
