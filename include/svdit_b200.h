@@ -162,6 +162,15 @@ int svd_attn_fwd(const svd_plan* plan, const void* q, const void* k, const void*
                  const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
                  int32_t dtype, void* stream);
 
+/* Per-head sum of squared differences in fp64 (numerics.py:114-121 mse, the
+ * search's reconstruction error, search.py:65-79): out[h] += sum over
+ * (b, n, c<d) of (a - b)^2 for bf16 [B, H, N, >=d] tensors given by element
+ * strides; b == NULL means zeros (the SKIP candidate).  out is a device
+ * double[H] the caller zeroes; divide by B*N*d for the MSE. */
+int svd_head_sqdiff(const void* a, const void* b, const int64_t* a_strides,
+                    const int64_t* b_strides, int32_t batch, int32_t heads, int64_t n_tokens,
+                    int32_t head_dim, double* out, void* stream);
+
 /* Scatter a gathered [world * max_rows, d] buffer of packed shard rows back
  * into O [B=1, H, N, d] (the multi-GPU reassembly after the NCCL all-gather). */
 int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, int64_t n_rows,

@@ -245,6 +245,44 @@ def sparse_attention_rows(q, k, v, active, bounds, qblocks) -> np.ndarray:
     return np.concatenate(outs, axis=2)
 
 
+def block_key_mass(q, k, grid: Grid) -> np.ndarray:
+    """attention.py:108-146: per-head attention mass on each key block,
+    streamed with the online-softmax recurrence, / N.  [B, H, nb] float64."""
+    q = np.asarray(q, dtype=np.float32)
+    B, H, N, d = q.shape
+    scale = 1.0 / np.sqrt(d)
+    bounds = grid.bounds
+    nb = len(bounds) - 1
+    q64 = q.astype(np.float64)
+    k64 = np.asarray(k, dtype=np.float32).astype(np.float64)
+    mass = np.zeros((B, H, nb))
+    for qb in range(nb):
+        r0, r1 = int(bounds[qb]), int(bounds[qb + 1])
+        rows = r1 - r0
+        m = np.full((B, H, rows), -np.inf)
+        l = np.zeros((B, H, rows))
+        partial = np.zeros((B, H, rows, nb))
+        for kb in range(nb):
+            c0, c1 = int(bounds[kb]), int(bounds[kb + 1])
+            s = np.matmul(q64[:, :, r0:r1], k64[:, :, c0:c1].swapaxes(-1, -2)) * scale
+            m_new = np.maximum(m, s.max(axis=-1))
+            p = np.exp(s - m_new[..., None])
+            alpha = np.exp(m - m_new)
+            block_total = p.sum(axis=-1)
+            l = l * alpha + block_total
+            partial *= alpha[..., None]
+            partial[:, :, :, kb] = block_total
+            m = m_new
+        mass += (partial / l[..., None]).sum(axis=2)
+    return mass / N
+
+
+def mse(a, b) -> float:
+    """numerics.py:114-121: fp64 mean squared difference."""
+    diff = np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64)
+    return float(np.mean(diff * diff)) if diff.size else 0.0
+
+
 def full_mask_attention(q, k, v, grid: Grid) -> np.ndarray:
     """attention.py:101-105."""
     nb = grid.n_blocks

@@ -40,6 +40,7 @@ from .patterns import (
 from .attention import (
     HeadGroup,
     LayerPlan,
+    block_key_mass,
     dense_attention,
     full_mask_attention,
     fused_layer_attention,

@@ -103,6 +103,11 @@ SIGNATURES = {
          POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
          c_int32, c_int32, c_int32, c_int32, c_void_p],
     ),
+    "svd_head_sqdiff": (
+        c_int,
+        [c_void_p, c_void_p, POINTER(c_int64), POINTER(c_int64), c_int32, c_int32, c_int64, c_int32,
+         c_void_p, c_void_p],
+    ),
     "svd_unpack_rows": (
         c_int,
         [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, POINTER(c_int64), c_int32, c_void_p],

@@ -408,7 +408,15 @@ def skip_attention(q, k, v):
     return _run(plan_for_assignment([skip_spec()] * H, _dense_layout(N)), q, k, v)
 
 
+def block_key_mass(q, k, grid: BlockGrid):
+    """Per-head attention mass per key block [B, H, nb] (attention.py:108-146);
+    computed on the GPU by calibrate.block_key_mass."""
+    from .calibrate import block_key_mass as _bkm
+
+    return _bkm(q, k, grid)
+
+
 __all__ = [
-    "LayerPlan", "HeadGroup", "group_heads", "fused_layer_attention", "sparse_attention",
+    "LayerPlan", "HeadGroup", "group_heads", "fused_layer_attention", "sparse_attention", "block_key_mass",
     "full_mask_attention", "dense_attention", "skip_attention", "plan_for_assignment",
 ]

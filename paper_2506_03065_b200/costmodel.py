@@ -74,6 +74,12 @@ class B200LatencyModel:
         }, indent=2) + "\n")
 
     @classmethod
+    def default(cls) -> "B200LatencyModel":
+        """The fitted model shipped in data/b200_latency.json (config-5 sweep)."""
+        path = Path(__file__).resolve().parent / "data" / "b200_latency.json"
+        return cls.load(path) if path.exists() else cls()
+
+    @classmethod
     def load(cls, path) -> "B200LatencyModel":
         obj = json.loads(Path(path).read_text())
         return cls(launch_ms=float(obj["launch_ms"]),

@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -606,6 +607,38 @@ __global__ void svd_unpack_kernel(const int32_t* __restrict__ row_head,
   reinterpret_cast<uint4*>(o + int64_t(h) * o_sh + int64_t(t) * o_sn)[c] = v;
 }
 
+// Per-head fp64 sum of squared differences (the search's MSE, numerics.py:114-121).
+__global__ void svd_sqdiff_kernel(const __nv_bfloat16* __restrict__ a,
+                                  const __nv_bfloat16* __restrict__ b, int64_t asb, int64_t ash,
+                                  int64_t asn, int64_t bsb, int64_t bsh, int64_t bsn, int B, int64_t N,
+                                  int d, double* __restrict__ out) {
+  const int h = blockIdx.y;
+  const int64_t rows = int64_t(B) * N;
+  double acc = 0.0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.y + threadIdx.y; r < rows;
+       r += int64_t(gridDim.x) * blockDim.y) {
+    const int bi = int(r / N);
+    const int64_t n = r % N;
+    const __nv_bfloat16* pa = a + bi * asb + h * ash + n * asn;
+    const __nv_bfloat16* pb = b ? b + bi * bsb + h * bsh + n * bsn : nullptr;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      const double x = double(__bfloat162float(pa[c])) - (pb ? double(__bfloat162float(pb[c])) : 0.0);
+      acc += x * x;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  __shared__ double part[32];
+  const int wid = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+  if ((threadIdx.x & 31) == 0) part[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    double t = 0.0;
+    const int nw = (blockDim.x * blockDim.y) >> 5;
+    for (int w = 0; w < nw; ++w) t += part[w];
+    atomicAdd(out + h, t);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -797,6 +830,23 @@ int svd_debug_trace(void* host, int64_t bytes, int32_t reset) {
   return e == cudaSuccess ? SVD_OK : cuda_fail(e, "trace");
 }
 #endif
+
+int svd_head_sqdiff(const void* a, const void* b, const int64_t* as, const int64_t* bs,
+                    int32_t batch, int32_t heads, int64_t n_tokens, int32_t head_dim, double* out,
+                    void* stream) {
+  if (!a || !out) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
+  if (batch < 1 || heads < 1 || n_tokens < 1 || head_dim < 1) return fail(SVD_ERR_SHAPE, "bad shape");
+  if (as[3] != 1 || (b && bs[3] != 1)) return fail(SVD_ERR_UNSUPPORTED, "head_dim stride must be 1");
+  const dim3 block(32, 8);
+  const int64_t rows = int64_t(batch) * n_tokens;
+  const dim3 grid(unsigned(std::min<int64_t>((rows + 7) / 8, 1024)), unsigned(heads));
+  svd_sqdiff_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b), as[0], as[1], as[2],
+      b ? bs[0] : 0, b ? bs[1] : 0, b ? bs[2] : 0, batch, n_tokens, head_dim, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "svd_sqdiff_kernel launch");
+  return SVD_OK;
+}
 
 int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, int64_t n_rows,
                     const void* packed, int64_t packed_row_stride, void* o, const int64_t* o_strides,

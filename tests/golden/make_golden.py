@@ -254,6 +254,16 @@ def attn_fixtures():
         data[f"fused{fi}_qscale"] = np.array(qscale)
         data[f"fused{fi}_specs"] = np.array([r + [0] * (width - len(r)) for r in rows], dtype=np.int64)
         data[f"fused{fi}_out"] = out
+    # block_key_mass (attention.py:108-146) — the stripe calibration input
+    from svdit.attention import block_key_mass
+
+    for bi, (lay, H, d, seed) in enumerate([((3, 4, 96, 32), 2, 16, 21), ((40, 3, 150, 64), 3, 32, 22)]):
+        layout = TokenLayout(*lay)
+        q, k, _ = random_qkv(seed, 1, H, layout.total_tokens, d)
+        q, k = bf16_round(q * np.float32(2.0)), bf16_round(k)
+        data[f"bkm{bi}_layout"] = np.array(lay, dtype=np.int64)
+        data[f"bkm{bi}_meta"] = np.array([H, d, seed], dtype=np.int64)
+        data[f"bkm{bi}_out"] = block_key_mass(q, k, block_grid(layout))
     np.savez_compressed(OUT / "golden_attn.npz", **data)
 
 

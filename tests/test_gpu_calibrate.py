@@ -1,0 +1,100 @@
+"""GPU calibration step vs the oracle: block_key_mass,
+stripe selection, per-head MSE and the four-candidate loss / mode choice of
+search.py:334-372."""
+
+import numpy as np
+import pytest
+
+import paper_2506_03065_b200 as S
+import svdit_oracle as O
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def _inputs(seed, h, n, d, qscale=2.0):
+    q, k, v = O.random_qkv(seed, 1, h, n, d)
+    return O.bf16_round(q * np.float32(qscale)), O.bf16_round(k), O.bf16_round(v)
+
+
+def test_block_key_mass_golden(golden_attn):
+    for bi in range(2):
+        lay = [int(x) for x in golden_attn[f"bkm{bi}_layout"]]
+        H, d, seed = (int(x) for x in golden_attn[f"bkm{bi}_meta"])
+        g = S.block_grid(S.TokenLayout(*lay))
+        q, k, _ = O.random_qkv(seed, 1, H, g.layout.total_tokens, d)
+        q, k = O.bf16_round(q * np.float32(2.0)), O.bf16_round(k)
+        got = S.block_key_mass(q, k, g)
+        want = golden_attn[f"bkm{bi}_out"]
+        assert got.shape == want.shape
+        np.testing.assert_allclose(got, want, rtol=0, atol=2e-3)
+        np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=5e-3)
+
+
+@pytest.mark.parametrize("lay,d", [((96, 16, 250, 64), 128), ((0, 16, 256, 64), 64)])
+def test_block_key_mass_vs_oracle_and_topk(lay, d):
+    og = O.block_grid(*lay)
+    q, k, _ = _inputs(5, 3, og.n, d, 3.0)
+    want = O.block_key_mass(q, k, og)
+    got = S.block_key_mass(q, k, S.block_grid(S.TokenLayout(*lay)))
+    np.testing.assert_allclose(got, want, rtol=0, atol=2e-3)
+    from paper_2506_03065_b200.calibrate import top_stripes
+
+    for h in range(3):
+        a, b = top_stripes(got[0, h], 2), top_stripes(want[0, h], 2)
+        order = np.sort(want[0, h])[::-1]
+        if order[1] - order[2] > 5e-3:  # clear margin: selection must agree
+            assert a == b
+
+
+def test_head_sqdiff_matches_fp64():
+    import torch
+
+    from paper_2506_03065_b200.calibrate import head_sqdiff
+
+    rng = np.random.default_rng(0)
+    a = O.bf16_round(rng.standard_normal((2, 3, 500, 64), dtype=np.float32))
+    b = O.bf16_round(rng.standard_normal((2, 3, 500, 64), dtype=np.float32))
+    ta, tb = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (a, b))
+    got = head_sqdiff(ta, tb).cpu().numpy()
+    want = ((a.astype(np.float64) - b) ** 2).sum(axis=(0, 2, 3))
+    np.testing.assert_allclose(got, want, rtol=1e-12)
+    np.testing.assert_allclose(head_sqdiff(ta).cpu().numpy(), (a.astype(np.float64) ** 2).sum(axis=(0, 2, 3)),
+                               rtol=1e-12)
+
+
+def test_candidate_evaluator_vs_oracle():
+    """Losses (MSE vs FULL + lam * density) within bf16 tolerance of the fp64
+    oracle; choices agree wherever the winning margin is clear."""
+    from paper_2506_03065_b200.calibrate import CandidateEvaluator
+
+    lay = (96, 16, 250, 64)
+    og = O.block_grid(*lay)
+    g = S.block_grid(S.TokenLayout(*lay))
+    H, d = 6, 64
+    q, k, v = _inputs(11, H, og.n, d, 4.0)
+    params = S.SearchParams(lam=0.05, epsilon=1.0)
+    ev = CandidateEvaluator(g, params)
+    res = ev.evaluate(q, k, v)
+    # oracle: same stripes (from the GPU's selection) so the candidates coincide
+    full = O.full_mask_attention(q, k, v, og)
+    pp = params.patterns
+    diag = O.sparse_attention(q, k, v, O.build_mask(pp.spec_for(S.Mode.DIAGONAL), og), og.bounds)
+    md = O.sparse_attention(q, k, v, O.build_mask(pp.spec_for(S.Mode.MULTI_DIAGONAL), og), og.bounds)
+    for h in range(H):
+        spec = pp.spec_for(S.Mode.VERTICAL_STRIPE, res.stripes[h])
+        st = O.sparse_attention(q[:, h:h + 1], k[:, h:h + 1], v[:, h:h + 1], O.build_mask(spec, og), og.bounds)
+        cands = [np.zeros_like(full[:, h:h + 1]), diag[:, h:h + 1], md[:, h:h + 1], st]
+        mses = [O.mse(c, full[:, h:h + 1]) for c in cands]
+        losses = [S.search.penalized_loss(m, s, params.lam) for m, s in zip(mses, res.sparsities[h])]
+        np.testing.assert_allclose(res.mse[h], mses, rtol=5e-2, atol=2e-6)
+        np.testing.assert_allclose(res.losses[h], losses, rtol=5e-2, atol=2e-6)
+        ranked = sorted(losses)
+        if ranked[1] - ranked[0] > 0.1 * ranked[0] and min(losses) <= params.epsilon:
+            assert res.choices[h] == S.select_mode(losses, res.sparsities[h], params.epsilon)
+    # the selected output carries each head's chosen candidate
+    sel = res.selected.float().cpu().numpy()
+    for h, ch in enumerate(res.choices):
+        if ch is S.Mode.SKIP:
+            assert not sel[:, h].any()

@@ -125,3 +125,15 @@ def test_bf16_round():
 
     want = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
     np.testing.assert_array_equal(O.bf16_round(x), want)
+
+
+def test_block_key_mass(golden_attn):
+    for bi in range(2):
+        lay = [int(x) for x in golden_attn[f"bkm{bi}_layout"]]
+        H, d, seed = (int(x) for x in golden_attn[f"bkm{bi}_meta"])
+        g = O.block_grid(*lay)
+        q, k, _ = O.random_qkv(seed, 1, H, g.n, d)
+        q, k = O.bf16_round(q * np.float32(2.0)), O.bf16_round(k)
+        got = O.block_key_mass(q, k, g)
+        np.testing.assert_allclose(got, golden_attn[f"bkm{bi}_out"], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=1e-9)
