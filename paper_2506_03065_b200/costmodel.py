@@ -44,24 +44,35 @@ def attention_latency_share(n_tokens: int, head_dim: int, heads: int, ffn_mult: 
 class B200LatencyModel:
     """Measured latency model of the fused sm_100a layer kernel.
 
-    t(ms) = launch_ms + tiles * ms_per_tile(d), where `tiles` is the number of
-    128x128 MMA tiles the plan issues (LayerPlan.info.computed_tiles) — the
-    quantity the kernel's time is linear in.  Coefficients are fitted from
-    the config-5 sweep (bench.py --sweep) and stored as JSON.
+    t(ms) = launch_ms + max(tiles * ms_per_tile(d), critical * ms_per_critical_tile(d))
+    where `tiles` is the number of 128x128 MMA tiles the plan issues
+    (LayerPlan.info.computed_tiles) and `critical` the tiles of its longest
+    work item: a launch is either throughput-bound (every SM busy) or bound
+    by its longest CTA (forced text/mixed query rows walk every key tile).
+    Coefficients come from the BASELINE config-5 sweep
+    (scripts/costmodel_sweep.py) and ship in data/b200_latency.json.
     """
 
     launch_ms: float = 0.01
-    ms_per_tile: dict = field(default_factory=lambda: {64: 5.0e-6, 128: 8.0e-6})
+    ms_per_tile: dict = field(default_factory=lambda: {64: 5.0e-6, 128: 7.4e-6})
+    ms_per_critical_tile: dict = field(default_factory=dict)
     source: str = "placeholder (not yet fitted)"
 
-    def predict_ms(self, computed_tiles: int, head_dim: int) -> float:
+    def predict_ms(self, computed_tiles: int, head_dim: int, critical_tiles: int = 0) -> float:
         per = self.ms_per_tile.get(int(head_dim))
         if per is None:
             raise ConfigError(f"no latency fit for head_dim {head_dim}")
-        return self.launch_ms + computed_tiles * per
+        crit = self.ms_per_critical_tile.get(int(head_dim), 0.0) * critical_tiles
+        return self.launch_ms + max(computed_tiles * per, crit)
+
+    def predict_plan_ms(self, plan, head_dim: int) -> float:
+        items, _ = plan.schedule()
+        crit = int(2 * items[:, 3].max()) if len(items) else 0
+        return self.predict_ms(plan.info.computed_tiles, head_dim, crit)
 
     def effective_sparsity(self, computed_tiles: int, full_tiles: int, head_dim: int) -> float:
-        """1 - t(pattern) / t(full): the latency-weighted sparsity for mode_loss."""
+        """1 - t(pattern) / t(full) on the throughput term: the latency-weighted
+        sparsity that drops into mode_loss's sparsity slot (search.py:65-79)."""
         t = self.predict_ms(computed_tiles, head_dim)
         t_full = self.predict_ms(full_tiles, head_dim)
         return min(1.0, max(0.0, 1.0 - t / t_full))
@@ -70,6 +81,7 @@ class B200LatencyModel:
         Path(path).write_text(json.dumps({
             "launch_ms": self.launch_ms,
             "ms_per_tile": {str(k): v for k, v in self.ms_per_tile.items()},
+            "ms_per_critical_tile": {str(k): v for k, v in self.ms_per_critical_tile.items()},
             "source": self.source,
         }, indent=2) + "\n")
 
@@ -84,4 +96,6 @@ class B200LatencyModel:
         obj = json.loads(Path(path).read_text())
         return cls(launch_ms=float(obj["launch_ms"]),
                    ms_per_tile={int(k): float(v) for k, v in obj["ms_per_tile"].items()},
+                   ms_per_critical_tile={int(k): float(v)
+                                         for k, v in obj.get("ms_per_critical_tile", {}).items()},
                    source=obj.get("source", str(path)))
