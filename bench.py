@@ -229,6 +229,9 @@ def run_ours(args):
     from paper_2506_03065_b200.sharding import HeadShardedLayer
 
     world, rank, local = init_dist()
+    # SVD_FORCE_DEVICE: test harness only — put every rank on one GPU (with
+    # SVD_BACKEND=gloo) to exercise the multi-rank path where one GPU exists
+    local = int(os.environ.get("SVD_FORCE_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = CONFIGS[args.config]

@@ -72,7 +72,11 @@ class HeadShardedLayer:
             kernel_events[1].record(stream)
         import torch.distributed as dist
 
-        dist.all_gather_into_tensor(self.gathered, self.packed)
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(self.gathered, self.packed)
+        else:  # gloo (CPU test harness): list form
+            dist.all_gather(list(self.gathered.view(self.world, self.max_rows, -1).unbind(0)),
+                            self.packed)
         ost = nat.i64x4(out.stride())
         nat.check(nat.lib().svd_unpack_rows(
             nat.c_void_p(self.row_head.data_ptr()), nat.c_void_p(self.row_token.data_ptr()),
