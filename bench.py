@@ -376,7 +376,7 @@ def run_ours(args):
             "ms_per_layer": round(e2e_ms, 3),
             "h2d_bytes_per_step": 3 * H * n * d * 2,
             "d2h_bytes_per_step": H * n * d * 2,
-            "path": "fused_layer_attention-equivalent public API (LayerPlan) with pinned host bf16 Q/K/V",
+            "path": "fused_layer_attention(pinned host bf16 Q/K/V): head-chunk pipelined H2D / kernel / D2H",
         },
         "gpu_launches": args.steps * (1 if world == 1 else 2),
         "clocks": clock,

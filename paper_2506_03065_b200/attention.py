@@ -8,9 +8,11 @@ fused_layer_attention (:186-212).
 
 Tensor contract.  Inputs are rank-4 [B, H, N, d].  CUDA torch tensors run
 in place (bf16 is used as is; other float dtypes are cast to bf16) and the
-result is a bf16 CUDA tensor.  NumPy inputs (the reference's own type) are
-moved to the current CUDA device, computed in bf16 and returned as float32
-NumPy arrays.  There is no CPU compute path: without a CUDA device the
+result is a bf16 CUDA tensor.  CPU torch tensors (ideally pinned bf16) are
+streamed through the GPU in head chunks with copy-in / compute / copy-out
+overlapped, and the result is a pinned CPU bf16 tensor.  NumPy inputs (the
+reference's own type) are moved to the current CUDA device, computed in bf16
+and returned as float32 NumPy arrays.  There is no CPU compute path: without a CUDA device the
 attention operators raise.
 """
 
@@ -43,6 +45,7 @@ class LayerPlan:
         self.n_heads = n_heads
         self.sharded = sharded
         self._dev_rows = None
+        self._sub = None
         self._finalizer = weakref.finalize(self, nat.lib().svd_plan_destroy, nat.c_void_p(handle))
 
     # -- construction
@@ -55,7 +58,10 @@ class LayerPlan:
         specs = (nat.SvdSpec * n)(*[nat.make_spec(s, keep) for s in assignment])
         out = nat.c_void_p()
         nat.check(nat.lib().svd_plan_create(nat.make_layout(layout), specs, n, nat.ctypes.byref(out)))
-        return cls(out.value, layout, n)
+        plan = cls(out.value, layout, n)
+        asg = list(assignment)
+        plan._sub = lambda h0, h1: cls.from_specs(asg[h0:h1], layout)
+        return plan
 
     @classmethod
     def from_masks(cls, layout: TokenLayout, group_masks, head_group) -> "LayerPlan":
@@ -74,7 +80,20 @@ class LayerPlan:
         nat.check(nat.lib().svd_plan_create_from_masks(
             nat.make_layout(layout), ng, nat.ptr(skip), nat.ptr(masks), nat.ptr(hg), int(hg.size),
             nat.ctypes.byref(out)))
-        return cls(out.value, layout, int(hg.size))
+        plan = cls(out.value, layout, int(hg.size))
+        gm = list(group_masks)
+        plan._sub = lambda h0, h1: cls.from_masks(layout, gm, hg[h0:h1])
+        return plan
+
+    def head_subplan(self, h0: int, h1: int) -> "LayerPlan":
+        """The plan restricted to heads [h0, h1) (cached): lets host-resident
+        layers be pipelined head-chunk by head-chunk."""
+        cache = self.__dict__.setdefault("_subplans", {})
+        if (h0, h1) not in cache:
+            if self._sub is None:
+                raise ConfigError("this plan cannot be split by heads")
+            cache[(h0, h1)] = self._sub(h0, h1)
+        return cache[(h0, h1)]
 
     # -- queries
     @property
@@ -248,11 +267,79 @@ def _to_device(xs):
     return out, was_numpy, dev
 
 
+HOST_CHUNKS = 4  # head chunks in the host-buffer pipeline
+
+
+def _run_host(plan: LayerPlan, q, k, v):
+    """Host (CPU torch) tensors: pipeline head chunks through copy-in,
+    compute and copy-out streams so the PCIe/C2C transfers overlap the kernel
+    (the end-to-end path of the operator with host buffers).  Returns a CPU
+    bf16 tensor (pinned)."""
+    import torch
+
+    B, H, N, d = q.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    D = _tensor_dim(d)
+    chunks = max(1, min(HOST_CHUNKS, H))
+    bounds = [round(i * H / chunks) for i in range(chunks + 1)]
+    out_host = torch.empty((B, H, N, d), dtype=torch.bfloat16, pin_memory=True)
+    compute = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    staged = []
+    with torch.cuda.stream(s_in):
+        for c in range(chunks):
+            h0, h1 = bounds[c], bounds[c + 1]
+            xs = []
+            for x in (q, k, v):
+                xc = x[:, h0:h1]
+                if xc.dtype != torch.bfloat16:
+                    xc = xc.to(torch.bfloat16)
+                if not xc.is_pinned():
+                    xc = xc.contiguous().pin_memory()
+                t = xc.to(dev, non_blocking=True)
+                if D != d:
+                    t = torch.nn.functional.pad(t, (0, D - d))
+                xs.append(t)
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+            staged.append((xs, ev))
+    done = []
+    for c in range(chunks):
+        h0, h1 = bounds[c], bounds[c + 1]
+        (qc, kc, vc), ev = staged[c]
+        compute.wait_event(ev)
+        oc = torch.empty((B, h1 - h0, N, D), dtype=torch.bfloat16, device=dev)
+        plan.head_subplan(h0, h1).forward(qc, kc, vc, oc, head_dim=d, stream=compute)
+        e2 = torch.cuda.Event()
+        e2.record(compute)
+        done.append((oc, e2))
+    with torch.cuda.stream(s_out):
+        for c in range(chunks):
+            h0, h1 = bounds[c], bounds[c + 1]
+            oc, e2 = done[c]
+            s_out.wait_event(e2)
+            out_host[:, h0:h1].copy_(oc[..., :d], non_blocking=True)
+            oc.record_stream(s_out)
+    for (xs, _), _o in zip(staged, done):
+        for t in xs:
+            t.record_stream(compute)
+    s_out.synchronize()  # a host result must be readable on return
+    return out_host
+
+
 def _run(plan: LayerPlan, q, k, v):
     import torch
 
     shape = _check_qkv(q, k, v)
     B, H, N, d = shape
+    if _is_torch(q) and q.device.type == "cpu":
+        if plan.layout.total_tokens != N:
+            raise ShapeError(f"mask grid covers {plan.layout.total_tokens} tokens, tensors have {N}")
+        if plan.n_heads != H:
+            raise ConfigError(f"plan covers {plan.n_heads} heads, tensors have {H}")
+        if not torch.cuda.is_available():
+            raise nat.NativeError("a CUDA device is required: the sm_100a kernel has no CPU path")
+        return _run_host(plan, q, k, v)
     if plan.layout.total_tokens != N:
         raise ShapeError(f"mask grid covers {plan.layout.total_tokens} tokens, tensors have {N}")
     if plan.n_heads != H:

@@ -91,13 +91,13 @@ class HeadShardedLayer:
 
         from .attention import fused_layer_attention
 
+        if self.shard is None:
+            # the public API with host buffers: head-chunk pipelined H2D / kernel / D2H
+            return fused_layer_attention(hq, hk, hv, groups)
         q = hq.to(self.device, non_blocking=True)
         k = hk.to(self.device, non_blocking=True)
         v = hv.to(self.device, non_blocking=True)
-        if self.shard is None:
-            out = fused_layer_attention(q, k, v, groups)
-        else:
-            out = torch.empty(hout.shape, dtype=torch.bfloat16, device=self.device)
-            self(q, k, v, out)
+        out = torch.empty(hout.shape, dtype=torch.bfloat16, device=self.device)
+        self(q, k, v, out)
         hout.copy_(out, non_blocking=True)
         return hout
