@@ -267,7 +267,7 @@ def _to_device(xs):
     return out, was_numpy, dev
 
 
-HOST_CHUNKS = 4  # head chunks in the host-buffer pipeline
+HOST_CHUNKS = 8  # head chunks in the host-buffer pipeline
 
 
 def _run_host(plan: LayerPlan, q, k, v):
