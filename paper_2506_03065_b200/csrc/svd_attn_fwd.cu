@@ -49,6 +49,9 @@ constexpr uint32_t kTmemCols = 512;
 #ifndef SVD_PINGPONG
 #define SVD_PINGPONG 0
 #endif
+#ifndef SVD_DYN_ISSUE
+#define SVD_DYN_ISSUE 0
+#endif
 
 template <int D>
 struct KCfg {
@@ -346,7 +349,67 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_s(1, 0);
         ptx::mma_commit(bar(C::kBarS + 1));
         ptx::mma_commit(bar(C::kBarKE + 0));
+#if SVD_DYN_ISSUE
+        if constexpr (!C::kEarlyS) {
+          // Dynamic issue: poll both tiles and issue whichever PV half / next S
+          // is ready, instead of a fixed A-then-B order that blocks on one
+          // tile's P while the other tile's work is ready.  Per tile: phase 0
+          // = PV half 0 of step jx (needs V_jx + P0), 1 = PV half 1 (needs P1),
+          // 2 = S(jx+1) (needs K_{jx+1}).  A V / K slot is released when both
+          // tiles are past it; the rings bound the drift between tiles.
+          int jx[2] = {0, 0}, ph[2] = {0, 0};
+          int pv_done[2] = {0, 0}, s_done[2] = {0, 0};
+          bool fin[2] = {false, false};
+          int ve_next = 0, ke_next = 1;  // next step whose V / K slot to release
+          while (!(fin[0] && fin[1])) {
+#pragma unroll 1
+            for (int x = 0; x < 2; ++x) {
+              if (fin[x]) continue;
+              const int j = jx[x];
+              if (ph[x] == 0) {
+                if (!ptx::mbar_try_wait(bar(C::kBarVF + j % C::kVSt), (j / C::kVSt) & 1)) continue;
+                if (!ptx::mbar_try_wait(bar(C::kBarP0 + x), j & 1)) continue;
+                ptx::tc_fence_after();
+                issue_pv_half(x, j % C::kVSt, 0, j > 0);
+                ph[x] = 1;
+              }
+              if (ph[x] == 1) {
+                if (!ptx::mbar_try_wait(bar(C::kBarP1 + x), j & 1)) continue;
+                ptx::tc_fence_after();
+                issue_pv_half(x, j % C::kVSt, 1, j > 0);
+                pv_done[x] = j + 1;
+                if (min(pv_done[0], pv_done[1]) > ve_next) {
+                  ptx::mma_commit(bar(C::kBarVE + ve_next % C::kVSt));
+                  ++ve_next;
+                }
+                if (j + 1 == n_kv) {
+                  ptx::mma_commit(bar(C::kBarO + x));
+                  fin[x] = true;
+                  continue;
+                }
+                ph[x] = 2;
+              }
+              if (ph[x] == 2) {
+                const int ks1 = (j + 1) % C::kKSt;
+                if (!ptx::mbar_try_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1)) continue;
+                ptx::tc_fence_after();
+                issue_s(x, ks1);
+                ptx::mma_commit(bar(C::kBarS + x));
+                s_done[x] = j + 1;
+                if (min(s_done[0], s_done[1]) >= ke_next) {
+                  ptx::mma_commit(bar(C::kBarKE + ke_next % C::kKSt));
+                  ++ke_next;
+                }
+                jx[x] = j + 1;
+                ph[x] = 0;
+              }
+            }
+          }
+        }
+        for (int j = 0; j < n_kv && C::kEarlyS; ++j) {
+#else
         for (int j = 0; j < n_kv; ++j) {
+#endif
           const int vs = j % C::kVSt;
           const int ks1 = (j + 1) % C::kKSt;
           const bool more = j + 1 < n_kv;
@@ -477,6 +540,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(bar(C::kBarSFree + x));  // S_X may now be overwritten by S_X(j+1)
     }
+#ifdef SVD_TRACE
+    if (tr) TRACE(x, tn, j, 3);  // S in registers
+#endif
     if (!(e.flags & kFlagAll)) apply_mask<FINE>(s, e, qslot, p, bits_row);
 
     // row max: 8 independent FMNMX chains, then a short tree
@@ -521,7 +587,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float mref = (m == -INFINITY) ? 0.f : m;
     const float2 nm = make_float2(-mref, -mref);
     const uint32_t tp = tmem + lane_off + C::col_p(x);
+#ifdef SVD_TRACE
+    if (tr) TRACE(x, tn, j, 4);  // max + rescale done
+#endif
     if (SVD_PINGPONG) named_bar_sync(2 + x, 256);  // wait for my turn
+#ifdef SVD_TRACE
+    if (tr) TRACE(x, tn, j, 5);  // turn acquired
+#endif
     float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                      make_float2(0.f, 0.f)};
 #pragma unroll
@@ -547,6 +619,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         if (c == 1) ptx::mbar_arrive(bar(C::kBarP0 + x));
+#ifdef SVD_TRACE
+        if (c == 1 && tr) TRACE(x, tn, j, 6);  // P half 0 handed over
+#endif
         if (c == 3) {
           if (!SVD_SPLIT_P) ptx::mbar_arrive(bar(C::kBarP0 + x));
           ptx::mbar_arrive(bar(C::kBarP1 + x));

@@ -50,6 +50,13 @@ for cta in range(8):
         wait = np.median([(ready[j] - before[j]) & 0xFFFFFFFF for j in js])
         per = np.median([(ready[j + 1] - ready[j]) & 0xFFFFFFFF for j in js])
         r[f"tile{x}"] = {"softmax_active": float(act), "wait_S": float(wait), "period": float(per)}
+        ph = {c: times(x, c) for c in (3, 4, 5, 6)}
+        def med(a, b):
+            v = [(b[j] - a[j]) & 0xFFFFFFFF for j in js if j in a and j in b]
+            return float(np.median(v)) if v else None
+        r[f"tile{x}"].update({"ready_to_loaded": med(ready, ph[3]), "loaded_to_max": med(ph[3], ph[4]),
+                              "turn_wait": med(ph[4], ph[5]), "exp_half0": med(ph[5], ph[6]),
+                              "exp_half1": med(ph[6], done)})
     m = ev.get(2, [])
     by = {}
     for c, j, cd in m:
