@@ -267,7 +267,7 @@ def _to_device(xs):
     return out, was_numpy, dev
 
 
-HOST_CHUNKS = int(__import__("os").environ.get("SVD_HOST_CHUNKS", "4"))  # head chunks, host pipeline
+HOST_CHUNKS = int(__import__("os").environ.get("SVD_HOST_CHUNKS", "6"))  # head chunks, host pipeline
 
 
 def _run_host(plan: LayerPlan, q, k, v):
