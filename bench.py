@@ -247,8 +247,18 @@ def run_ours(args):
     q = torch.randn(1, H, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
     k = torch.randn(1, H, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
     v = torch.randn(1, H, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
-    layer = HeadShardedLayer(plan, world, rank, head_dim=d, device=dev)
-    out = torch.empty(1, H, n, d, device=dev, dtype=torch.bfloat16)
+    # N>1: the fused path (shard kernel stores rows into every rank's O over
+    # peer memory) unless SVD_MULTI_GPU=nccl selects packed rows + NCCL
+    # all-gather + unpack
+    mgpu = os.environ.get("SVD_MULTI_GPU", "p2p") if world > 1 else "single"
+    if mgpu == "p2p":
+        from paper_2506_03065_b200.sharding import PeerShardedLayer
+
+        layer = PeerShardedLayer(plan, world, rank, d, dev, (1, H, n, d))
+        out = layer.out
+    else:
+        layer = HeadShardedLayer(plan, world, rank, head_dim=d, device=dev)
+        out = torch.empty(1, H, n, d, device=dev, dtype=torch.bfloat16)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -350,7 +360,10 @@ def run_ours(args):
             "heads": H, "head_dim": d, "batch": 1,
             "mode_mix_F_S_D_MD_VS": cfg["mix"],
             "density": round(f_active / f_dense, 4),
-            "parallelism": f"head/q-range sharded x{world} + NCCL all-gather" if world > 1 else "1 GPU",
+            "parallelism": ({"p2p": f"head/q-range sharded x{world}, rows stored to every rank's O "
+                                    "from the kernel epilogue over peer memory",
+                             "nccl": f"head/q-range sharded x{world} + NCCL all-gather + unpack",
+                             "single": "1 GPU"}[mgpu]),
             "l2": "inputs 3 x %.0f MB bf16 > 126 MB L2: no flush" % (H * n * d * 2 / 1e6),
         },
         "ms_per_layer": round(ms, 4),
@@ -378,7 +391,7 @@ def run_ours(args):
             "d2h_bytes_per_step": H * n * d * 2,
             "path": "fused_layer_attention(pinned host bf16 Q/K/V): head-chunk pipelined H2D / kernel / D2H",
         },
-        "gpu_launches": args.steps * (1 if world == 1 else 2),
+        "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),
         "clocks": clock,
     }
     if not args.no_cpu_baseline:

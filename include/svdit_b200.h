@@ -162,6 +162,26 @@ int svd_attn_fwd(const svd_plan* plan, const void* q, const void* k, const void*
                  const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
                  int32_t dtype, void* stream);
 
+/* Fused compute + reassembly for multi-GPU: as svd_attn_fwd, but every
+ * output row the plan (typically a svd_plan_shard view) produces is stored
+ * into all n_peers O buffers — this rank's and its peers' [B, H, N,
+ * tensor_dim] outputs mapped into this process (CUDA IPC / NVLink P2P) —
+ * straight from the kernel epilogue, so no separate all-gather or unpack
+ * runs on the data path.  All peers share o_strides.  n_peers <= 8. */
+int svd_attn_fwd_peers(const svd_plan* plan, const void* q, const void* k, const void* v,
+                       void* const* o_peers, int32_t n_peers, const int64_t* q_strides,
+                       const int64_t* k_strides, const int64_t* v_strides,
+                       const int64_t* o_strides, int32_t batch, int32_t head_dim,
+                       int32_t tensor_dim, int32_t dtype, void* stream);
+
+/* CUDA IPC helpers for svd_attn_fwd_peers: export a device pointer as a
+ * 64-byte handle + byte offset into its allocation; import a peer's handle
+ * on the CURRENT device (peer access enabled lazily) and get the pointer;
+ * close an imported mapping (pass the pointer svd_ipc_import returned). */
+int svd_ipc_export(const void* ptr, uint8_t* handle64, int64_t* offset);
+int svd_ipc_import(const uint8_t* handle64, int64_t offset, void** ptr);
+int svd_ipc_close(void* ptr, int64_t offset);
+
 /* Per-head sum of squared differences in fp64 (numerics.py:114-121 mse, the
  * search's reconstruction error, search.py:65-79): out[h] += sum over
  * (b, n, c<d) of (a - b)^2 for bf16 [B, H, N, >=d] tensors given by element

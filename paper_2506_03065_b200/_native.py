@@ -103,6 +103,15 @@ SIGNATURES = {
          POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
          c_int32, c_int32, c_int32, c_int32, c_void_p],
     ),
+    "svd_attn_fwd_peers": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+         POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
+         c_int32, c_int32, c_int32, c_int32, c_void_p],
+    ),
+    "svd_ipc_export": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
+    "svd_ipc_import": (c_int, [c_void_p, c_int64, POINTER(c_void_p)]),
+    "svd_ipc_close": (c_int, [c_void_p, c_int64]),
     "svd_head_sqdiff": (
         c_int,
         [c_void_p, c_void_p, POINTER(c_int64), POINTER(c_int64), c_int32, c_int32, c_int64, c_int32,

@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "svd_plan.h"
@@ -35,6 +36,7 @@
 namespace svd {
 
 constexpr int kThreads = 384;
+constexpr int kMaxPeers = 8;
 constexpr uint32_t kTmemCols = 512;
 
 #ifndef SVD_EARLY_S
@@ -105,7 +107,22 @@ struct FwdParams {
   int n_blocks;
   int packed;                // shard plan: O is a packed [rows, d] buffer
   float scale_log2;          // log2(e) / sqrt(d)
+  // Fused reassembly: when n_peers > 0 every output row is stored into all
+  // n_peers O buffers (this rank's and its peers', mapped over NVLink), all
+  // with the same [B, H, N, D] strides; `o` / `packed` are then unused.
+  int n_peers;
+  __nv_bfloat16* peer_o[kMaxPeers];
 };
+
+// Store one 16-byte chunk of an output row: to o + off, or to every peer.
+__device__ __forceinline__ void store_row16(const FwdParams& p, int64_t off, const uint4& val) {
+  if (p.n_peers == 0) {
+    *reinterpret_cast<uint4*>(p.o + off) = val;
+  } else {
+#pragma unroll 1
+    for (int r = 0; r < p.n_peers; ++r) *reinterpret_cast<uint4*>(p.peer_o[r] + off) = val;
+  }
+}
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -481,18 +498,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int qseg = itp->qseg[2 * x + (row >> 6)];
   const int tok_r = qseg * kSeg + (row & 63);
   const bool row_valid = qseg >= 0 && tok_r < p.n_tokens;
-  __nv_bfloat16* orow;
-  if (p.packed)
-    orow = p.o + (int64_t(itp->out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
+  // element offset of this thread's output row (in O, the packed buffer, or
+  // every peer's O)
+  int64_t orow;
+  if (p.packed && p.n_peers == 0)
+    orow = (int64_t(itp->out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
   else
-    orow = p.o + int64_t(b) * p.o_sb + int64_t(head) * p.o_sh + int64_t(tok_r) * p.o_sn;
+    orow = int64_t(b) * p.o_sb + int64_t(head) * p.o_sh + int64_t(tok_r) * p.o_sn;
 
   if (n_kv == 0) {
     // SKIP head (attention.py:51-54): exact zeros, no scores, no softmax
     if (row_valid) {
-      uint4 z = make_uint4(0, 0, 0, 0);
+      const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) reinterpret_cast<uint4*>(orow)[c] = z;
+      for (int c = 0; c < D / 8; ++c) store_row16(p, orow + c * 8, z);
     }
     named_bar_sync(1, 32 + 256);
     return;
@@ -655,12 +674,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
     if (row_valid) {
-      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        store_row16(p, orow + c * 32 + i * 8,
+                    make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
     }
   }
+  if (p.n_peers > 0) __threadfence_system();  // peer rows visible before the kernel retires
   ptx::tc_fence_before();
   named_bar_sync(1, 32 + 256);
 }
@@ -807,7 +827,7 @@ template <int D>
 static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const void* k,
                       const void* v, void* o, const int64_t* qs, const int64_t* ks,
                       const int64_t* vs, const int64_t* os, int32_t batch, int32_t head_dim,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0) {
   using C = KCfg<D>;
   CUtensorMap mq, mk, mv;
   const int64_t N = P->grid.n, H = P->n_heads;
@@ -842,6 +862,8 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   prm.n_blocks = int(P->grid.nb);
   prm.packed = P->sharded ? 1 : 0;
   prm.scale_log2 = float(1.4426950408889634 / std::sqrt(double(head_dim)));
+  prm.n_peers = n_peers;
+  for (int r = 0; r < n_peers; ++r) prm.peer_o[r] = static_cast<__nv_bfloat16*>(peers[r]);
   if (T->n_items == 0) return SVD_OK;
   dim3 grid(unsigned(T->n_items), unsigned(batch));
   if (P->fine)
@@ -905,6 +927,82 @@ int svd_debug_trace(void* host, int64_t bytes, int32_t reset) {
   return e == cudaSuccess ? SVD_OK : cuda_fail(e, "trace");
 }
 #endif
+
+int svd_ipc_export(const void* ptr, uint8_t* handle64, int64_t* offset) {
+  if (!ptr || !handle64 || !offset) return fail(SVD_ERR_CONFIG, "NULL argument");
+  static PFN_cuMemGetAddressRange_v3020 range_fn = nullptr;
+  if (!range_fn) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(SVD_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range_fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(SVD_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, 64);
+  *offset = int64_t(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return SVD_OK;
+}
+
+int svd_ipc_import(const uint8_t* handle64, int64_t offset, void** ptr) {
+  if (!handle64 || !ptr) return fail(SVD_ERR_CONFIG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *ptr = static_cast<uint8_t*>(base) + offset;
+  return SVD_OK;
+}
+
+int svd_ipc_close(void* ptr, int64_t offset) {
+  if (!ptr) return SVD_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(static_cast<uint8_t*>(ptr) - offset);
+  return e == cudaSuccess ? SVD_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+int svd_attn_fwd_peers(const svd_plan* P, const void* q, const void* k, const void* v,
+                       void* const* o_peers, int32_t n_peers, const int64_t* q_strides,
+                       const int64_t* k_strides, const int64_t* v_strides,
+                       const int64_t* o_strides, int32_t batch, int32_t head_dim,
+                       int32_t tensor_dim, int32_t dtype, void* stream) {
+  if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
+  if (dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
+  if (n_peers < 1 || n_peers > kMaxPeers || !o_peers)
+    return fail(SVD_ERR_CONFIG, "n_peers must be in [1, " + std::to_string(kMaxPeers) + "]");
+  if (head_dim < 1 || head_dim > tensor_dim)
+    return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
+  if (batch < 1) return fail(SVD_ERR_SHAPE, "batch must be >= 1");
+  if (!q || !k || !v) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
+  if (o_strides[3] != 1 || (o_strides[2] * 2) % 16 != 0)
+    return fail(SVD_ERR_UNSUPPORTED, "o: rows must be contiguous and 16-byte aligned");
+  for (int r = 0; r < n_peers; ++r)
+    if (!o_peers[r] || (reinterpret_cast<uintptr_t>(o_peers[r]) & 15) != 0)
+      return fail(SVD_ERR_UNSUPPORTED, "peer O pointers must be non-NULL and 16-byte aligned");
+  DeviceTables* T = nullptr;
+  int st = ensure_device_tables(P, &T);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (tensor_dim) {
+    case 64:
+      return launch_fwd<64>(P, T, q, k, v, o_peers[0], q_strides, k_strides, v_strides, o_strides,
+                            batch, head_dim, s, o_peers, n_peers);
+    case 128:
+      return launch_fwd<128>(P, T, q, k, v, o_peers[0], q_strides, k_strides, v_strides, o_strides,
+                             batch, head_dim, s, o_peers, n_peers);
+    default:
+      return fail(SVD_ERR_UNSUPPORTED,
+                  "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
+  }
+}
 
 int svd_head_sqdiff(const void* a, const void* b, const int64_t* as, const int64_t* bs,
                     int32_t batch, int32_t heads, int64_t n_tokens, int32_t head_dim, double* out,

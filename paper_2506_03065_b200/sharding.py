@@ -33,6 +33,92 @@ def gathered_row_maps(plan: LayerPlan, world: int):
     return shards, heads, toks, max_rows
 
 
+class PeerShardedLayer:
+    """One layer over `world` ranks with the reassembly fused into the kernel.
+
+    Every rank owns an O buffer [1, H, N, D]; the buffers are exchanged once
+    as CUDA IPC handles over the process group and mapped into every rank
+    (NVLink peer memory between GPUs).  Each rank launches its shard of the
+    plan with svd_attn_fwd_peers: the kernel epilogue stores each finished
+    row into all `world` O buffers, so the transfer overlaps the attention
+    math tile by tile and no all-gather / unpack runs afterwards.  A
+    stream sync + process-group barrier closes the step (every rank's O is
+    then complete).
+    """
+
+    def __init__(self, plan: LayerPlan, world: int, rank: int, head_dim: int, device, shape):
+        import torch
+        import torch.distributed as dist
+
+        self.plan = plan
+        self.world = world
+        self.rank = rank
+        self.head_dim = head_dim
+        self.device = device
+        self.shard = plan.shard(world, rank) if world > 1 else plan
+        self.out = torch.empty(shape, dtype=torch.bfloat16, device=device)
+        off = nat.c_int64(0)
+        buf = (nat.c_uint8 * 64)()
+        nat.check(nat.lib().svd_ipc_export(nat.c_void_p(self.out.data_ptr()), buf, nat.ctypes.byref(off)))
+        handle = bytes(buf)
+        gathered = [None] * world
+        if world > 1:
+            dist.all_gather_object(gathered, (rank, handle, int(off.value)))
+        else:
+            gathered = [(rank, handle, int(off.value))]
+        self._opened = []
+        ptrs = []
+        for r, h, o in sorted(gathered):
+            if r == rank:
+                ptrs.append(self.out.data_ptr())
+                continue
+            p = nat.c_void_p()
+            hb = (nat.c_uint8 * 64).from_buffer_copy(h)
+            nat.check(nat.lib().svd_ipc_import(hb, o, nat.ctypes.byref(p)))
+            self._opened.append((p.value, o))
+            ptrs.append(p.value)
+        self.peer_ptrs = (nat.c_void_p * world)(*ptrs)
+
+    def __call__(self, q, k, v, out=None, kernel_events=None):
+        """Run this rank's shard; returns this rank's complete O (all rows)."""
+        import torch
+
+        stream = torch.cuda.current_stream(self.device)
+        if kernel_events is not None:
+            kernel_events[0].record(stream)
+        st = [nat.i64x4(t.stride()) for t in (q, k, v)]
+        nat.check(nat.lib().svd_attn_fwd_peers(
+            self.shard.handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
+            nat.c_void_p(v.data_ptr()), self.peer_ptrs, self.world, st[0], st[1], st[2],
+            nat.i64x4(self.out.stride()), 1, int(self.head_dim), int(q.shape[-1]), 0,
+            nat.c_void_p(stream.cuda_stream)))
+        if kernel_events is not None:
+            kernel_events[1].record(stream)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            stream.synchronize()
+            dist.barrier()
+        if out is not None and out.data_ptr() != self.out.data_ptr():
+            out.copy_(self.out)
+        return self.out
+
+    def e2e(self, hq, hk, hv, hout, groups=None):
+        """End-to-end step from pinned host buffers: H2D, fused shard kernel
+        (rows land in every rank's O), D2H of the full O."""
+        q = hq.to(self.device, non_blocking=True)
+        k = hk.to(self.device, non_blocking=True)
+        v = hv.to(self.device, non_blocking=True)
+        out = self(q, k, v)
+        hout.copy_(out, non_blocking=True)
+        return hout
+
+    def close(self):
+        for p, o in self._opened:
+            nat.lib().svd_ipc_close(nat.c_void_p(p), o)
+        self._opened = []
+
+
 class HeadShardedLayer:
     """Callable running one layer's attention on `world` ranks (1 = plain launch)."""
 

@@ -1,0 +1,82 @@
+"""Fused compute + reassembly over peer memory (svd_attn_fwd_peers): two
+ranks (processes) map each other's O buffers via CUDA IPC; each rank's shard
+kernel stores its rows into both buffers.  On a one-GPU box both processes
+share the device (the NVLink path differs only in where the peer memory
+lives).  Every rank's O must equal the single-launch layer output bit for
+bit, step after step."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2506_03065_b200 as S
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, path, d):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_03065_b200.sharding import PeerShardedLayer
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        lay = (96, 16, 250, 64)
+        specs = [S.full_spec(), S.diagonal_spec(1), S.skip_spec(), S.multi_diagonal_spec(),
+                 S.vertical_stripe_spec(stripes=(5, 33)), S.full_spec()]
+        gen = torch.Generator().manual_seed(3)
+        q, k, v = (torch.randn(1, len(specs), 4096, d, generator=gen).to(torch.bfloat16).to(dev)
+                   for _ in range(3))
+        plan = S.LayerPlan.from_specs(specs, S.TokenLayout(*lay))
+        ref = torch.empty_like(q)
+        plan.forward(q, k, v, ref, head_dim=d)
+        layer = PeerShardedLayer(plan, world, rank, d, dev, tuple(q.shape))
+        oks = []
+        for _ in range(2):
+            layer.out.fill_(float("nan"))
+            dist.barrier()
+            out = layer(q, k, v)
+            torch.cuda.synchronize()
+            oks.append(bool(torch.equal(out, ref)))
+        dist.barrier()
+        layer.close()
+        torch.save({"ok": oks}, f"{path}.{rank}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d", [128, 64])
+def test_peer_fused_reassembly_two_ranks(tmp_path, d):
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path / "r"), d), nprocs=2, join=True)
+    res = [torch.load(f"{tmp_path / 'r'}.{r}") for r in range(2)]
+    assert all(all(r["ok"]) for r in res), res
+
+
+def test_peer_single_rank_equals_plain_launch():
+    from paper_2506_03065_b200.sharding import PeerShardedLayer
+
+    dev = torch.device("cuda", 0)
+    specs = [S.diagonal_spec(1), S.full_spec(), S.skip_spec()]
+    plan = S.LayerPlan.from_specs(specs, S.TokenLayout(20, 4, 250, 64))
+    q, k, v = (torch.randn(1, 3, 1020, 128, device=dev).to(torch.bfloat16) for _ in range(3))
+    ref = torch.empty_like(q)
+    plan.forward(q, k, v, ref, head_dim=128)
+    layer = PeerShardedLayer(plan, 1, 0, 128, dev, tuple(q.shape))
+    assert torch.equal(layer(q, k, v), ref)
+    assert np.isfinite(layer.out.float().cpu().numpy()).all()
