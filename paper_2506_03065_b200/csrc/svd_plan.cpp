@@ -12,6 +12,7 @@
 // list of 128-key tiles (pairs of key segments) plus per-tile activity bits.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -216,7 +217,7 @@ static inline bool bit_of(const std::vector<uint64_t>& bits, int64_t i) {
 // residue classes), then the remainder in index order (diagonal bands and
 // stripes, whose neighbouring rows overlap).
 static std::vector<std::array<int32_t, kSlotsPerItem>> cluster_segments(
-    const std::vector<std::vector<uint64_t>>& keyset, int64_t nseg) {
+    const std::vector<std::vector<uint64_t>>& keyset, int64_t nseg, int csize) {
   std::map<std::vector<uint64_t>, std::vector<int32_t>> buckets;
   std::vector<const std::vector<uint64_t>*> order;
   for (int64_t s = 0; s < nseg; ++s) {
@@ -231,18 +232,19 @@ static std::vector<std::array<int32_t, kSlotsPerItem>> cluster_segments(
   std::vector<int32_t> rest;
   for (auto* key : order) {
     const auto& members = buckets[*key];
-    size_t full = members.size() / kSlotsPerItem * kSlotsPerItem;
-    for (size_t i = 0; i < full; i += kSlotsPerItem) {
+    size_t full = members.size() / csize * csize;
+    for (size_t i = 0; i < full; i += csize) {
       std::array<int32_t, kSlotsPerItem> q;
-      for (int k = 0; k < kSlotsPerItem; ++k) q[k] = members[i + k];
+      for (int k = 0; k < kSlotsPerItem; ++k) q[k] = k < csize ? members[i + k] : -1;
       out.push_back(q);
     }
     for (size_t i = full; i < members.size(); ++i) rest.push_back(members[i]);
   }
   std::sort(rest.begin(), rest.end());
-  for (size_t i = 0; i < rest.size(); i += kSlotsPerItem) {
+  for (size_t i = 0; i < rest.size(); i += csize) {
     std::array<int32_t, kSlotsPerItem> q;
-    for (int k = 0; k < kSlotsPerItem; ++k) q[k] = i + k < rest.size() ? rest[i + k] : -1;
+    for (int k = 0; k < kSlotsPerItem; ++k)
+      q[k] = (k < csize && i + k < rest.size()) ? rest[i + k] : -1;
     out.push_back(q);
   }
   return out;
@@ -254,9 +256,10 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
   grp.qgroup_kv_begin.clear();
   grp.qgroup_kv_count.clear();
   if (grp.skip) {
-    for (int64_t s = 0; s < nseg; s += kSlotsPerItem) {
+    for (int64_t s = 0; s < nseg; s += P->cluster) {
       std::array<int32_t, kSlotsPerItem> q;
-      for (int k = 0; k < kSlotsPerItem; ++k) q[k] = s + k < nseg ? int32_t(s + k) : -1;
+      for (int k = 0; k < kSlotsPerItem; ++k)
+        q[k] = (k < P->cluster && s + k < nseg) ? int32_t(s + k) : -1;
       grp.qgroups.push_back(q);
       grp.qgroup_kv_begin.push_back(0);
       grp.qgroup_kv_count.push_back(0);
@@ -265,7 +268,7 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
   }
   std::vector<std::vector<uint64_t>> keyset;
   segment_keysets(grp, P->grid, nseg, &keyset);
-  grp.qgroups = cluster_segments(keyset, nseg);
+  grp.qgroups = cluster_segments(keyset, nseg, P->cluster);
   const bool tail_partial = (P->grid.n % kSeg) != 0;
   const int64_t words = (nseg + 63) / 64;
   std::vector<uint64_t> uni(words);
@@ -317,7 +320,17 @@ static double group_active_pairs(const Group& grp, const Grid& g) {
   return total;
 }
 
+// Query segments per CTA: 4 (two 128-row tiles ping-ponging, the default
+// kernel) or 2 (one 128-row tile with double-buffered S).  SVD_CLUSTER
+// overrides the default.
+static int default_cluster() {
+  const char* env = std::getenv("SVD_CLUSTER");
+  if (env && (std::atoi(env) == 2 || std::atoi(env) == 4)) return std::atoi(env);
+  return kDefaultCluster;
+}
+
 static void finalize_plan(svd_plan* P) {
+  if (P->cluster == 0) P->cluster = default_cluster();
   P->nseg = (P->grid.n + kSeg - 1) / kSeg;
   P->fine = (P->grid.bs % kSeg) != 0;
   P->kv.clear();
@@ -601,6 +614,7 @@ int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** sh
   S->nseg = P->nseg;
   S->n_heads = P->n_heads;
   S->fine = P->fine;
+  S->cluster = P->cluster;
   S->head_group = P->head_group;
   S->groups = P->groups;
   S->kv = P->kv;
