@@ -187,6 +187,14 @@ class LayerPlan:
             int(batch), hd, int(d_t), 0, nat.c_void_p(stream.cuda_stream)))
 
 
+def _cluster_key():
+    """Kernel-variant selector the native planner reads (SVD_CLUSTER); part of
+    every plan-cache key so a variant switch never reuses a stale plan."""
+    import os
+
+    return os.environ.get("SVD_CLUSTER", "")
+
+
 _PLAN_CACHE: "OrderedDict[tuple, LayerPlan]" = OrderedDict()
 _PLAN_CACHE_MAX = 64
 
@@ -195,7 +203,7 @@ def plan_for_assignment(assignment, layout: TokenLayout) -> LayerPlan:
     """Cached native plan for (layout, per-head specs).  The reference rebuilds
     every mask on every call (attention.py:178-182); the plan is immutable, so
     one build per distinct assignment suffices."""
-    key = (layout, tuple(assignment))
+    key = (layout, tuple(assignment), _cluster_key())
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         plan = LayerPlan.from_specs(list(assignment), layout)
@@ -387,7 +395,7 @@ def group_heads(assignment, grid: BlockGrid) -> list[HeadGroup]:
     the returned groups share that plan, so fused_layer_attention launches it
     without rebuilding anything."""
     assignment = list(assignment)
-    key = (grid.layout, tuple(assignment))
+    key = (grid.layout, tuple(assignment), _cluster_key())
     cached = _GROUP_CACHE.get(key)
     if cached is not None:
         _GROUP_CACHE.move_to_end(key)
