@@ -302,11 +302,13 @@ def run_ours(args):
     for _ in range(2):
         layer.e2e(hq, hk, hv, hout, groups)
     barrier()
-    te = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_walls = []
     e0.record(stream)
     for _ in range(e2e_steps):
+        w0 = time.perf_counter()
         layer.e2e(hq, hk, hv, hout, groups)
+        e2e_walls.append(round((time.perf_counter() - w0) * 1e3, 2))
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
@@ -387,6 +389,7 @@ def run_ours(args):
             "value": round(f_dense / (e2e_ms * 1e-3) / 1e12, 2),
             "unit": "TFLOP/s (effective, dense-equivalent)",
             "ms_per_layer": round(e2e_ms, 3),
+            "wall_ms_steps": e2e_walls,
             "h2d_bytes_per_step": 3 * H * n * d * 2,
             "d2h_bytes_per_step": H * n * d * 2,
             "path": "fused_layer_attention(pinned host bf16 Q/K/V): head-chunk pipelined H2D / kernel / D2H",

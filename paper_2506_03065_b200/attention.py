@@ -187,14 +187,6 @@ class LayerPlan:
             int(batch), hd, int(d_t), 0, nat.c_void_p(stream.cuda_stream)))
 
 
-def _cluster_key():
-    """Kernel-variant selector the native planner reads (SVD_CLUSTER); part of
-    every plan-cache key so a variant switch never reuses a stale plan."""
-    import os
-
-    return os.environ.get("SVD_CLUSTER", "")
-
-
 _PLAN_CACHE: "OrderedDict[tuple, LayerPlan]" = OrderedDict()
 _PLAN_CACHE_MAX = 64
 
@@ -203,7 +195,7 @@ def plan_for_assignment(assignment, layout: TokenLayout) -> LayerPlan:
     """Cached native plan for (layout, per-head specs).  The reference rebuilds
     every mask on every call (attention.py:178-182); the plan is immutable, so
     one build per distinct assignment suffices."""
-    key = (layout, tuple(assignment), _cluster_key())
+    key = (layout, tuple(assignment))
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         plan = LayerPlan.from_specs(list(assignment), layout)
@@ -278,11 +270,50 @@ def _to_device(xs):
 HOST_CHUNKS = int(__import__("os").environ.get("SVD_HOST_CHUNKS", "6"))  # head chunks, host pipeline
 
 
-def _run_host(plan: LayerPlan, q, k, v):
+class _Staging:
+    """Device staging for the host-buffer path, owned by a plan and reused
+    across calls: Q/K/V/O at the kernel's head width (zero padding written
+    once), the copy-in / copy-out streams, and a lock (one host call at a
+    time per plan and device)."""
+
+    def __init__(self, dev, B: int, H: int, N: int, D: int):
+        import threading
+
+        import torch
+
+        self.qkv = [torch.zeros((B, H, N, D), dtype=torch.bfloat16, device=dev) for _ in range(3)]
+        self.o = torch.empty((B, H, N, D), dtype=torch.bfloat16, device=dev)
+        self.s_in, self.s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self.lock = threading.Lock()
+
+
+def _host_staging(plan: "LayerPlan", dev, B: int, N: int, d: int, D: int) -> _Staging:
+    cache = plan.__dict__.setdefault("_staging", {})
+    key = (dev.index, B, N, d, D)  # d too: columns [d, D) must stay the zeros written once
+    st = cache.get(key)
+    if st is None:
+        cache.clear()  # one resident staging set per plan
+        st = cache[key] = _Staging(dev, B, plan.n_heads, N, D)
+    return st
+
+
+def _check_out(out, shape, device_type: str):
+    import torch
+
+    if not _is_torch(out) or out.dtype != torch.bfloat16 or tuple(out.shape) != tuple(shape):
+        raise ShapeError(f"out must be a bf16 torch tensor of shape {tuple(shape)}")
+    if out.device.type != device_type:
+        raise ShapeError(f"out must live on the {device_type} like q/k/v")
+    if out.stride(-1) != 1:
+        raise ShapeError("out must have a unit-stride last dimension")
+
+
+def _run_host(plan: LayerPlan, q, k, v, out=None):
     """Host (CPU torch) tensors: pipeline head chunks through copy-in,
     compute and copy-out streams so the PCIe/C2C transfers overlap the kernel
     (the end-to-end path of the operator with host buffers).  Returns a CPU
-    bf16 tensor (pinned)."""
+    bf16 tensor (pinned), or writes `out` (a caller-owned, ideally pinned, CPU
+    bf16 tensor: no per-call host allocation)."""
     import torch
 
     B, H, N, d = q.shape
@@ -290,52 +321,48 @@ def _run_host(plan: LayerPlan, q, k, v):
     D = _tensor_dim(d)
     chunks = max(1, min(HOST_CHUNKS, H))
     bounds = [round(i * H / chunks) for i in range(chunks + 1)]
-    out_host = torch.empty((B, H, N, d), dtype=torch.bfloat16, pin_memory=True)
-    compute = torch.cuda.current_stream(dev)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    staged = []
-    with torch.cuda.stream(s_in):
+    if out is None:
+        out_host = torch.empty((B, H, N, d), dtype=torch.bfloat16, pin_memory=True)
+    else:
+        _check_out(out, (B, H, N, d), "cpu")
+        out_host = out
+    st = _host_staging(plan, dev, B, N, d, D)
+    with st.lock:
+        compute = torch.cuda.current_stream(dev)
+        s_in, s_out = st.s_in, st.s_out
+        loaded = []
+        with torch.cuda.stream(s_in):
+            for c in range(chunks):
+                h0, h1 = bounds[c], bounds[c + 1]
+                for x, buf in zip((q, k, v), st.qkv):
+                    xc = x[:, h0:h1]
+                    if xc.dtype != torch.bfloat16:
+                        xc = xc.to(torch.bfloat16)
+                    if not xc.is_pinned():
+                        xc = xc.contiguous().pin_memory()
+                    buf[:, h0:h1, :, :d].copy_(xc, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_in)
+                loaded.append(ev)
+        computed = []
         for c in range(chunks):
             h0, h1 = bounds[c], bounds[c + 1]
-            xs = []
-            for x in (q, k, v):
-                xc = x[:, h0:h1]
-                if xc.dtype != torch.bfloat16:
-                    xc = xc.to(torch.bfloat16)
-                if not xc.is_pinned():
-                    xc = xc.contiguous().pin_memory()
-                t = xc.to(dev, non_blocking=True)
-                if D != d:
-                    t = torch.nn.functional.pad(t, (0, D - d))
-                xs.append(t)
+            compute.wait_event(loaded[c])
+            qc, kc, vc = (buf[:, h0:h1] for buf in st.qkv)
+            plan.head_subplan(h0, h1).forward(qc, kc, vc, st.o[:, h0:h1], head_dim=d, stream=compute)
             ev = torch.cuda.Event()
-            ev.record(s_in)
-            staged.append((xs, ev))
-    done = []
-    for c in range(chunks):
-        h0, h1 = bounds[c], bounds[c + 1]
-        (qc, kc, vc), ev = staged[c]
-        compute.wait_event(ev)
-        oc = torch.empty((B, h1 - h0, N, D), dtype=torch.bfloat16, device=dev)
-        plan.head_subplan(h0, h1).forward(qc, kc, vc, oc, head_dim=d, stream=compute)
-        e2 = torch.cuda.Event()
-        e2.record(compute)
-        done.append((oc, e2))
-    with torch.cuda.stream(s_out):
-        for c in range(chunks):
-            h0, h1 = bounds[c], bounds[c + 1]
-            oc, e2 = done[c]
-            s_out.wait_event(e2)
-            out_host[:, h0:h1].copy_(oc[..., :d], non_blocking=True)
-            oc.record_stream(s_out)
-    for (xs, _), _o in zip(staged, done):
-        for t in xs:
-            t.record_stream(compute)
-    s_out.synchronize()  # a host result must be readable on return
+            ev.record(compute)
+            computed.append(ev)
+        with torch.cuda.stream(s_out):
+            for c in range(chunks):
+                h0, h1 = bounds[c], bounds[c + 1]
+                s_out.wait_event(computed[c])
+                out_host[:, h0:h1].copy_(st.o[:, h0:h1, :, :d], non_blocking=True)
+        s_out.synchronize()  # a host result must be readable on return
     return out_host
 
 
-def _run(plan: LayerPlan, q, k, v):
+def _run(plan: LayerPlan, q, k, v, out=None):
     import torch
 
     shape = _check_qkv(q, k, v)
@@ -347,13 +374,24 @@ def _run(plan: LayerPlan, q, k, v):
             raise ConfigError(f"plan covers {plan.n_heads} heads, tensors have {H}")
         if not torch.cuda.is_available():
             raise nat.NativeError("a CUDA device is required: the sm_100a kernel has no CPU path")
-        return _run_host(plan, q, k, v)
+        return _run_host(plan, q, k, v, out)
     if plan.layout.total_tokens != N:
         raise ShapeError(f"mask grid covers {plan.layout.total_tokens} tokens, tensors have {N}")
     if plan.n_heads != H:
         raise ConfigError(f"plan covers {plan.n_heads} heads, tensors have {H}")
+    if out is not None and not _is_torch(q):
+        raise ShapeError("out= is supported for torch tensors only")
     (qt, kt, vt), was_numpy, dev = _to_device((q, k, v))
     dt = qt.shape[-1]
+    if out is not None:
+        _check_out(out, (B, H, N, d), "cuda")
+        if dt == d and all((st * 2) % 16 == 0 for st in out.stride()[:-1]) and out.data_ptr() % 16 == 0:
+            plan.forward(qt, kt, vt, out, head_dim=d)
+        else:
+            tmp = torch.empty((B, H, N, dt), dtype=torch.bfloat16, device=dev)
+            plan.forward(qt, kt, vt, tmp, head_dim=d)
+            out.copy_(tmp[..., :d])
+        return out
     out = torch.empty((B, H, N, dt), dtype=torch.bfloat16, device=dev)
     plan.forward(qt, kt, vt, out, head_dim=d)
     if dt != d:
@@ -395,7 +433,7 @@ def group_heads(assignment, grid: BlockGrid) -> list[HeadGroup]:
     the returned groups share that plan, so fused_layer_attention launches it
     without rebuilding anything."""
     assignment = list(assignment)
-    key = (grid.layout, tuple(assignment), _cluster_key())
+    key = (grid.layout, tuple(assignment))
     cached = _GROUP_CACHE.get(key)
     if cached is not None:
         _GROUP_CACHE.move_to_end(key)
@@ -445,8 +483,12 @@ def _plan_for_groups(groups, H: int, N: int) -> LayerPlan:
     return LayerPlan.from_masks(layout, masks, head_group)
 
 
-def fused_layer_attention(q, k, v, groups):
-    """One layer's attention, every head in one kernel launch (attention.py:186-212)."""
+def fused_layer_attention(q, k, v, groups, out=None):
+    """One layer's attention, every head in one kernel launch (attention.py:186-212).
+
+    `out` (extension; torch tensors only): a caller-owned bf16 result buffer
+    on the device of q/k/v (a CPU one for host tensors, ideally pinned), written
+    in place and returned — a serving loop then allocates nothing per call."""
     B, H, N, d = _check_qkv(q, k, v)
     seen: list[int] = []
     for g in groups:
@@ -457,7 +499,7 @@ def fused_layer_attention(q, k, v, groups):
         if g.mask is not None and g.mask.grid.layout.total_tokens != N:
             raise ShapeError(
                 f"mask grid covers {g.mask.grid.layout.total_tokens} tokens, tensors have {N}")
-    return _run(_plan_for_groups(groups, H, N), q, k, v)
+    return _run(_plan_for_groups(groups, H, N), q, k, v, out)
 
 
 _MASK_PLANS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()

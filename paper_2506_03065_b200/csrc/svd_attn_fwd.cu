@@ -51,6 +51,12 @@ constexpr uint32_t kTmemCols = 512;
 #ifndef SVD_PINGPONG
 #define SVD_PINGPONG 0
 #endif
+// Row sums over the bf16-rounded P (the values the PV MMA consumes) rather
+// than the fp32 exps: numerator and denominator then see the same weights,
+// which removes the bf16 rounding of the dominant weight from peaked rows.
+#ifndef SVD_SUM_ROUNDED
+#define SVD_SUM_ROUNDED 1
+#endif
 #ifndef SVD_DYN_ISSUE
 #define SVD_DYN_ISSUE 0
 #endif
@@ -195,14 +201,6 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
 #endif
 template <int D>
 constexpr int kEmuPairs = D == 128 ? SVD_EMU128 : SVD_EMU64;
-#ifndef SVD_EMU1_128
-#define SVD_EMU1_128 0
-#endif
-#ifndef SVD_EMU1_64
-#define SVD_EMU1_64 0
-#endif
-template <int D>
-constexpr int kEmuPairs1 = D == 128 ? SVD_EMU1_128 : SVD_EMU1_64;  // one-tile kernel
 
 #ifdef SVD_TRACE
 // Debug-only pipeline trace: (clock, step<<8 | event) pairs for the first 8
@@ -317,11 +315,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
       if (lane == 0 && n_kv > 0) {
+        // smem / TMEM bases laundered once per KV step (asm barrier below):
+        // stops ptxas hoisting every stage's descriptors out of the loop and
+        // spilling them to local memory under the kernel-wide register cap
+        uint32_t sb = base, tb = tmem;
         constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false);
         constexpr uint32_t id_pv = ptx::idesc_bf16(128, D, true);
         auto issue_s = [&](int x, int ks) {
-          const uint32_t qb = base + C::kOffQ + x * C::kTileBytes;
-          const uint32_t kb = base + C::kOffK + ks * C::kTileBytes;
+          const uint32_t qb = sb + C::kOffQ + x * C::kTileBytes;
+          const uint32_t kb = sb + C::kOffK + ks * C::kTileBytes;
 #if SVD_SPLIT_S
           constexpr uint32_t id_s64 = ptx::idesc_bf16(128, 64, false);
 #pragma unroll
@@ -329,25 +331,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
-              ptx::mma_ss(tmem + C::col_s(x) + hh * 64, ptx::sw128_desc(qb + off, 16, 1024),
+              ptx::mma_ss(tb + C::col_s(x) + hh * 64, ptx::sw128_desc(qb + off, 16, 1024),
                           ptx::sw128_desc(kb + off + hh * 8192, 16, 1024), id_s64, kk > 0);
             }
 #else
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
-            ptx::mma_ss(tmem + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
+            ptx::mma_ss(tb + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
                         ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
           }
 #endif
         };
         // O_X += P_X V_j, keys [64*half, 64*half + 64): four K=16 steps
         auto issue_pv_half = [&](int x, int vs, int half, bool acc) {
-          const uint32_t vb = base + C::kOffV + vs * C::kTileBytes;
+          const uint32_t vb = sb + C::kOffV + vs * C::kTileBytes;
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = half * 4 + k4;
-            ptx::mma_ts(tmem + C::col_o(x), tmem + C::col_p(x) + kk * 8,
+            ptx::mma_ts(tb + C::col_o(x), tb + C::col_p(x) + kk * 8,
                         ptx::sw128_desc(vb + kk * 2048, C::kSlabBytes, 1024), id_pv,
                         (acc || kk > 0) ? 1u : 0u);
           }
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
         for (int j = 0; j < n_kv; ++j) {
 #endif
+          asm volatile("" : "+r"(sb), "+r"(tb));
           const int vs = j % C::kVSt;
           const int ks1 = (j + 1) % C::kKSt;
           const bool more = j + 1 < n_kv;
@@ -636,8 +639,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           pv.x = ptx::ex2(xv.x);
           pv.y = ptx::ex2(xv.y);
         }
-        acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
         pk[i] = ptx::pack_bf16(pv.x, pv.y);
+        if (SVD_SUM_ROUNDED) ptx::acc_bf16x2(acc[i & 3], pk[i]);
+        else acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
       }
       ptx::tmem_st16(tp + c * 16, pk);
       if ((c == 1 && SVD_SPLIT_P) || c == 3) {
@@ -691,325 +695,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.n_peers > 0) __threadfence_system();  // peer rows visible before the kernel retires
   ptx::tc_fence_before();
   named_bar_sync(1, 32 + 256);
-}
-
-// ------------------------------------------------------------------------
-// One-tile variant (plan cluster = 2): a CTA owns ONE 128-row Q tile and
-// double-buffers S in TMEM (S0, S1: 128 fp32 columns each; O: D columns; 384
-// of 512 columns even at d=128).  S(j+1) is computed while the softmax works
-// on S(j); P(j) aliases S buffer j%2, so S(j+2) is issued after PV(j) (the
-// tensor pipe executes in issue order).  The softmax warpgroup never waits on
-// its own PV -> S chain.
-template <int D>
-struct K1Cfg {
-  static constexpr int kSlabs = D / 64;
-  static constexpr int kBoxBytes = 64 * 64 * 2;
-  static constexpr int kSlabBytes = 128 * 128;
-  static constexpr int kTileBytes = 128 * D * 2;
-  static constexpr int kKSt = D == 128 ? 3 : 4;
-  static constexpr int kVSt = D == 128 ? 3 : 4;
-  static constexpr int kOffQ = 0;
-  static constexpr int kOffK = kTileBytes;
-  static constexpr int kOffV = kOffK + kKSt * kTileBytes;
-  static constexpr int kOffBar = kOffV + kVSt * kTileBytes;
-  static constexpr int kBarQ = 0;
-  static constexpr int kBarKF = 1;
-  static constexpr int kBarKE = kBarKF + kKSt;
-  static constexpr int kBarVF = kBarKE + kKSt;
-  static constexpr int kBarVE = kBarVF + kVSt;
-  static constexpr int kBarSF = kBarVE + kVSt;   // [2] S buffer full
-  static constexpr int kBarP0 = kBarSF + 2;
-  static constexpr int kBarP1 = kBarP0 + 1;
-  static constexpr int kBarO = kBarP1 + 1;
-  static constexpr int kBarPVD = kBarO + 1;      // PV(j) complete
-  static constexpr int kNumBars = kBarPVD + 1;
-  static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
-  static constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;
-  __device__ static constexpr uint32_t col_s(int buf) { return buf ? 128u : 0u; }
-  static constexpr uint32_t kColO = 256u;
-};
-
-constexpr int kThreads1 = 256;
-
-template <int D, bool FINE>
-__global__ void __launch_bounds__(kThreads1, 1)
-    svd_fwd1_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
-  using C = K1Cfg<D>;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = ptx::smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* base_ptr = smem_raw + (base - raw);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  auto bar = [&](int i) { return base + C::kOffBar + 8u * uint32_t(i); };
-
-  const WorkItem* itp = p.items + blockIdx.x;
-  const int b = blockIdx.y;
-  const int n_kv = itp->kv_count;
-  const int head = itp->head;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(bar(C::kBarQ), 1);
-    for (int i = 0; i < C::kKSt; ++i) {
-      ptx::mbar_init(bar(C::kBarKF + i), 1);
-      ptx::mbar_init(bar(C::kBarKE + i), 1);
-    }
-    for (int i = 0; i < C::kVSt; ++i) {
-      ptx::mbar_init(bar(C::kBarVF + i), 1);
-      ptx::mbar_init(bar(C::kBarVE + i), 1);
-    }
-    ptx::mbar_init(bar(C::kBarSF + 0), 1);
-    ptx::mbar_init(bar(C::kBarSF + 1), 1);
-    ptx::mbar_init(bar(C::kBarP0), 128);
-    ptx::mbar_init(bar(C::kBarP1), 128);
-    ptx::mbar_init(bar(C::kBarO), 1);
-    ptx::mbar_init(bar(C::kBarPVD), 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) {
-    ptx::tmem_alloc(base + C::kOffTmemSlot, kTmemCols);
-    ptx::tmem_relinquish();
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(base_ptr + C::kOffTmemSlot);
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && n_kv > 0) {
-      ptx::prefetch_tmap(&tm_q);
-      ptx::prefetch_tmap(&tm_k);
-      ptx::prefetch_tmap(&tm_v);
-      const uint64_t pol_q = ptx::policy_evict_first();
-      const uint64_t pol_kv = ptx::policy_evict_last();
-      const int s0 = itp->qseg[0], s1 = itp->qseg[1] >= 0 ? itp->qseg[1] : itp->qseg[0];
-      ptx::mbar_arrive_expect_tx(bar(C::kBarQ), C::kTileBytes);
-      load_tile<D>(&tm_q, base + C::kOffQ, bar(C::kBarQ), s0, s1, head, b, pol_q);
-      const KvEntry* kvp = p.kv + itp->kv_begin;
-      for (int j = 0; j < n_kv; ++j) {
-        const KvEntry e = load_kv(kvp + j);
-        const int k0 = e.kseg0, k1 = e.kseg1 >= 0 ? e.kseg1 : e.kseg0;
-        const int ks = j % C::kKSt, vs = j % C::kVSt;
-        ptx::mbar_wait(bar(C::kBarKE + ks), ((j / C::kKSt) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(bar(C::kBarKF + ks), C::kTileBytes);
-        load_tile<D>(&tm_k, base + C::kOffK + ks * C::kTileBytes, bar(C::kBarKF + ks), k0, k1, head,
-                     b, pol_kv);
-        ptx::mbar_wait(bar(C::kBarVE + vs), ((j / C::kVSt) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(bar(C::kBarVF + vs), C::kTileBytes);
-        load_tile<D>(&tm_v, base + C::kOffV + vs * C::kTileBytes, bar(C::kBarVF + vs), k0, k1, head,
-                     b, pol_kv);
-      }
-    }
-    __syncwarp();
-    return;
-  }
-
-  if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n_kv > 0) {
-      constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false);
-      constexpr uint32_t id_pv = ptx::idesc_bf16(128, D, true);
-      auto issue_s = [&](int buf, int ks) {
-        const uint32_t qb = base + C::kOffQ;
-        const uint32_t kb = base + C::kOffK + ks * C::kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
-          ptx::mma_ss(tmem + C::col_s(buf), ptx::sw128_desc(qb + off, 16, 1024),
-                      ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
-        }
-      };
-      auto issue_pv_half = [&](int buf, int vs, int half, bool acc) {
-        const uint32_t vb = base + C::kOffV + vs * C::kTileBytes;
-#pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
-          const int kk = half * 4 + k4;
-          ptx::mma_ts(tmem + C::kColO, tmem + C::col_s(buf) + kk * 8,
-                      ptx::sw128_desc(vb + kk * 2048, C::kSlabBytes, 1024), id_pv,
-                      (acc || kk > 0) ? 1u : 0u);
-        }
-      };
-      ptx::mbar_wait(bar(C::kBarQ), 0);
-      for (int j = 0; j < 2 && j < n_kv; ++j) {
-        ptx::mbar_wait(bar(C::kBarKF + j), 0);
-        ptx::tc_fence_after();
-        issue_s(j, j);
-        ptx::mma_commit(bar(C::kBarSF + j));
-        ptx::mma_commit(bar(C::kBarKE + j));
-      }
-      for (int j = 0; j < n_kv; ++j) {
-        const int buf = j & 1;
-        const int vs = j % C::kVSt;
-        ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
-        ptx::mbar_wait(bar(C::kBarP0), j & 1);
-        ptx::tc_fence_after();
-        issue_pv_half(buf, vs, 0, j > 0);
-        ptx::mbar_wait(bar(C::kBarP1), j & 1);
-        ptx::tc_fence_after();
-        issue_pv_half(buf, vs, 1, j > 0);
-        ptx::mma_commit(bar(C::kBarVE + vs));
-        ptx::mma_commit(bar(C::kBarPVD));
-        if (j + 1 == n_kv) ptx::mma_commit(bar(C::kBarO));
-        if (j + 2 < n_kv) {
-          const int ks = (j + 2) % C::kKSt;
-          ptx::mbar_wait(bar(C::kBarKF + ks), ((j + 2) / C::kKSt) & 1);
-          ptx::tc_fence_after();
-          issue_s(buf, ks);  // buffer j%2: after PV(j) in issue order
-          ptx::mma_commit(bar(C::kBarSF + buf));
-          ptx::mma_commit(bar(C::kBarKE + ks));
-        }
-      }
-    }
-    __syncwarp();
-    named_bar_sync(1, 32 + 128);
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTmemCols);
-    return;
-  }
-
-  if (warp < 4) return;  // warps 2-3: no role
-
-  // -------------------------------------------------------------- softmax / epilogue
-  const int wq = warp & 3;
-  const int row = wq * 32 + lane;
-  const uint32_t lane_off = uint32_t(wq * 32) << 16;
-  const int qslot = row >> 6;
-  const int qseg = itp->qseg[qslot];
-  const int tok_r = qseg * kSeg + (row & 63);
-  const bool row_valid = qseg >= 0 && tok_r < p.n_tokens;
-  int64_t orow;
-  if (p.packed && p.n_peers == 0)
-    orow = (int64_t(itp->out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
-  else
-    orow = int64_t(b) * p.o_sb + int64_t(head) * p.o_sh + int64_t(tok_r) * p.o_sn;
-
-  if (n_kv == 0) {
-    if (row_valid) {
-      const uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int c = 0; c < D / 8; ++c) store_row16(p, orow + c * 8, z);
-    }
-    named_bar_sync(1, 32 + 128);
-    return;
-  }
-
-  const uint32_t* bits_row = nullptr;
-  if constexpr (FINE) {
-    const int qb = min(max(tok_r, 0) / p.block_size, p.n_blocks - 1);
-    bits_row = p.bits + p.bit_off[itp->group] + int64_t(qb) * p.words_per_row;
-  }
-  const float sl2 = p.scale_log2;
-  const float2 sl2x2 = make_float2(sl2, sl2);
-  float m = -INFINITY;
-  float l = 0.f;
-  const KvEntry* kvp = p.kv + itp->kv_begin;
-  KvEntry e_next = load_kv(kvp);
-
-  for (int j = 0; j < n_kv; ++j) {
-    const int buf = j & 1;
-    const KvEntry e = e_next;
-    if (j + 1 < n_kv) e_next = load_kv(kvp + j + 1);
-    ptx::mbar_wait(bar(C::kBarSF + buf), (j >> 1) & 1);
-    ptx::tc_fence_after();
-    float s[128];
-    const uint32_t ts = tmem + lane_off + C::col_s(buf);
-    ptx::tmem_ld32(ts + 0, *reinterpret_cast<float(*)[32]>(&s[0]));
-    ptx::tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-    ptx::tmem_ld32(ts + 64, *reinterpret_cast<float(*)[32]>(&s[64]));
-    ptx::tmem_ld32(ts + 96, *reinterpret_cast<float(*)[32]>(&s[96]));
-    ptx::tmem_wait_ld();
-    if (!(e.flags & kFlagAll)) apply_mask<FINE>(s, e, qslot, p, bits_row);
-
-    float mp[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) mp[t] = fmaxf(s[t], s[8 + t]);
-#pragma unroll
-    for (int i = 16; i < 128; i += 16)
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mp[t] = fmaxf(mp[t], fmaxf(s[i + t], s[i + 8 + t]));
-    const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
-                           fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
-    const float m_new = fmaxf(m, mx * sl2);
-    const bool resc = m_new > m + 8.0f;
-    if (__any_sync(0xffffffffu, resc)) {
-      const float alpha = resc ? ptx::ex2(m - m_new) : 1.0f;
-      if (j > 0) {
-        // O must hold PV(j-1) before it is rescaled (S(j) no longer implies it)
-        ptx::mbar_wait(bar(C::kBarPVD), (j - 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t to = tmem + lane_off + C::kColO;
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          float ov[32];
-          ptx::tmem_ld32(to + c * 32, ov);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] *= alpha;
-          ptx::tmem_st32(to + c * 32, ov);
-        }
-      }
-      if (resc) {
-        l *= alpha;
-        m = m_new;
-      }
-    }
-    const float mref = (m == -INFINITY) ? 0.f : m;
-    const float2 nm = make_float2(-mref, -mref);
-    const uint32_t tp = tmem + lane_off + C::col_s(buf);
-    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                     make_float2(0.f, 0.f)};
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float2 xv = ptx::ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sl2x2, nm);
-        float2 pv;
-        if ((i & 7) >= 8 - kEmuPairs1<D>) {
-          pv = ptx::ex2_poly2(xv);
-        } else {
-          pv.x = ptx::ex2(xv.x);
-          pv.y = ptx::ex2(xv.y);
-        }
-        acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
-        pk[i] = ptx::pack_bf16(pv.x, pv.y);
-      }
-      ptx::tmem_st16(tp + c * 16, pk);
-      if (c == 1 || c == 3) {
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(bar(c == 1 ? C::kBarP0 : C::kBarP1));
-      }
-    }
-    const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
-    const float2 a = ptx::fadd2(a01, a23);
-    l += a.x + a.y;
-  }
-
-  ptx::mbar_wait(bar(C::kBarO), 0);
-  ptx::tc_fence_after();
-  const float inv = l > 0.f ? 1.0f / l : 0.f;
-  const uint32_t to = tmem + lane_off + C::kColO;
-#pragma unroll
-  for (int c = 0; c < D / 32; ++c) {
-    float ov[32];
-    ptx::tmem_ld32(to + c * 32, ov);
-    ptx::tmem_wait_ld();
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
-    if (row_valid) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        store_row16(p, orow + c * 32 + i * 8,
-                    make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
-    }
-  }
-  if (p.n_peers > 0) __threadfence_system();
-  ptx::tc_fence_before();
-  named_bar_sync(1, 32 + 128);
 }
 
 // Multi-GPU reassembly: packed shard rows -> O[0, head, token, :]
@@ -1162,7 +847,6 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   if ((st = make_tmap(&mq, q, qs, batch, H, N, D, "q"))) return st;
   if ((st = make_tmap(&mk, k, ks, batch, H, N, D, "k"))) return st;
   if ((st = make_tmap(&mv, v, vs, batch, H, N, D, "v"))) return st;
-  using C1 = K1Cfg<D>;
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1172,12 +856,6 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(svd_fwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                C::kSmemBytes);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(svd_fwd1_kernel<D, false>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmemBytes);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(svd_fwd1_kernel<D, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmemBytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     attr_set[dev] = true;
   }
@@ -1200,12 +878,7 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   for (int r = 0; r < n_peers; ++r) prm.peer_o[r] = static_cast<__nv_bfloat16*>(peers[r]);
   if (T->n_items == 0) return SVD_OK;
   dim3 grid(unsigned(T->n_items), unsigned(batch));
-  if (P->cluster == 2) {
-    if (P->fine)
-      svd_fwd1_kernel<D, true><<<grid, kThreads1, C1::kSmemBytes, stream>>>(mq, mk, mv, prm);
-    else
-      svd_fwd1_kernel<D, false><<<grid, kThreads1, C1::kSmemBytes, stream>>>(mq, mk, mv, prm);
-  } else if (P->fine) {
+  if (P->fine) {
     svd_fwd_kernel<D, true><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);
   } else {
     svd_fwd_kernel<D, false><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);

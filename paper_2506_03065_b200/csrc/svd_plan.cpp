@@ -320,17 +320,10 @@ static double group_active_pairs(const Group& grp, const Grid& g) {
   return total;
 }
 
-// Query segments per CTA: 4 (two 128-row tiles ping-ponging, the default
-// kernel) or 2 (one 128-row tile with double-buffered S).  SVD_CLUSTER
-// overrides the default.
-static int default_cluster() {
-  const char* env = std::getenv("SVD_CLUSTER");
-  if (env && (std::atoi(env) == 2 || std::atoi(env) == 4)) return std::atoi(env);
-  return kDefaultCluster;
-}
 
 static void finalize_plan(svd_plan* P) {
-  if (P->cluster == 0) P->cluster = default_cluster();
+  // query segments per CTA: two 128-row tiles ping-ponging in the kernel
+  if (P->cluster == 0) P->cluster = kDefaultCluster;
   P->nseg = (P->grid.n + kSeg - 1) / kSeg;
   P->fine = (P->grid.bs % kSeg) != 0;
   P->kv.clear();

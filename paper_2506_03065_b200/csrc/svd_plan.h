@@ -18,7 +18,7 @@ namespace svd {
 // block_size-64 blocks map 1:1 onto segments (layout.py:31 default).
 constexpr int kSeg = 64;
 constexpr int kSlotsPerItem = 4;  // two 128-row Q tiles (A, B) x two segments
-constexpr int kDefaultCluster = 4;  // query segments per CTA (4 or 2), see svd_plan.cpp
+constexpr int kDefaultCluster = 4;  // query segments per CTA (two 128-row tiles)
 
 // KvEntry.flags
 constexpr uint32_t kFlagAll = 1u << 8;    // every present (q slot, k slot) active, no tail
@@ -105,7 +105,7 @@ struct svd_plan {
   int64_t computed_tiles = 0;
   // shard view
   bool sharded = false;
-  int32_t cluster = 0;  // query segments per work item: 4 (two tiles) or 2 (one tile)
+  int32_t cluster = 0;  // query segments per work item (kDefaultCluster)
   int64_t n_rows = 0;
   std::vector<int32_t> row_head, row_token;
   // device copies, per CUDA device ordinal

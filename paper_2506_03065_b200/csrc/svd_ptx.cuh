@@ -186,6 +186,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+// acc += the two bf16 halves of a packed pair, widened exactly (sm_100a mixed-
+// precision FADD: one FHADD.BF16 per half).  Summing the ROUNDED P keeps the
+// softmax denominator consistent with the P that enters the PV MMA.
+__device__ __forceinline__ void acc_bf16x2(float2& acc, uint32_t pk) {
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+      "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y)
+      : "r"(pk));
+}
 // 2^x for a pair on the FMA pipe (offloads the MUFU unit): round-to-nearest
 // range reduction with the 1.5*2^23 trick, near-minimax cubic for 2^f on
 // [-0.5, 0.5] (max rel. error 7.5e-5, far below bf16's 2^-9), exponent add.

@@ -179,7 +179,7 @@ class HeadShardedLayer:
 
         if self.shard is None:
             # the public API with host buffers: head-chunk pipelined H2D / kernel / D2H
-            return fused_layer_attention(hq, hk, hv, groups)
+            return fused_layer_attention(hq, hk, hv, groups, out=hout)
         q = hq.to(self.device, non_blocking=True)
         k = hk.to(self.device, non_blocking=True)
         v = hv.to(self.device, non_blocking=True)

@@ -1,5 +1,6 @@
-"""Time the host-buffer public API path (pinned bf16 Q/K/V in, O out) for
-head-chunk counts given on the command line."""
+"""Time the host-buffer public API path (pinned bf16 Q/K/V in, O out) per
+step, with a fresh pinned result per call and with a caller-owned pinned out=
+buffer, for head-chunk counts given on the command line."""
 import json
 import sys
 import time
@@ -18,23 +19,18 @@ layout = S.TokenLayout(*cfg["layout"])
 n, H, d = layout.total_tokens, cfg["heads"], cfg["d"]
 groups = S.group_heads(bench.assignment_for(cfg, S), S.block_grid(layout))
 q, k, v = (torch.randn(1, H, n, d).to(torch.bfloat16).pin_memory() for _ in range(3))
+hout = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
 res = {}
-for chunks in [int(c) for c in (sys.argv[2:] or ["1", "2", "4", "8"])]:
+for chunks in [int(c) for c in (sys.argv[2:] or ["4", "6", "8"])]:
     A.HOST_CHUNKS = chunks
-    for _ in range(2):
-        S.fused_layer_attention(q, k, v, groups)
-    ts = []
-    for _ in range(4):
-        t0 = time.perf_counter()
-        S.fused_layer_attention(q, k, v, groups)
-        ts.append((time.perf_counter() - t0) * 1e3)
-    res[chunks] = round(sorted(ts)[len(ts) // 2], 2)
-# raw transfer rates for reference
-x = torch.empty(3 * H * n * d, dtype=torch.bfloat16).pin_memory()
-y = torch.empty_like(x, device="cuda")
-torch.cuda.synchronize()
-t0 = time.perf_counter(); y.copy_(x, non_blocking=True); torch.cuda.synchronize()
-h2d = x.numel() * 2 / (time.perf_counter() - t0) / 1e9
-t0 = time.perf_counter(); x.copy_(y, non_blocking=True); torch.cuda.synchronize()
-d2h = x.numel() * 2 / (time.perf_counter() - t0) / 1e9
-print(json.dumps({"e2e_ms_by_chunks": res, "h2d_GBps": round(h2d, 1), "d2h_GBps": round(d2h, 1)}))
+    for mode in ("alloc", "out"):
+        kw = {"out": hout} if mode == "out" else {}
+        for _ in range(2):
+            S.fused_layer_attention(q, k, v, groups, **kw)
+        ts = []
+        for _ in range(6):
+            t0 = time.perf_counter()
+            S.fused_layer_attention(q, k, v, groups, **kw)
+            ts.append(round((time.perf_counter() - t0) * 1e3, 1))
+        res[f"{chunks}_{mode}"] = ts
+print(json.dumps({"e2e_wall_ms": res}))

@@ -1,8 +1,10 @@
 """Randomised parity fuzz: random layouts (text / frame borders / partial
 tails, block sizes that are and are not multiples of 64), head dims, batch
-sizes, mixes of all five modes with random geometry, both storage orders and
-both kernel variants (cluster 4 default, cluster 2 one-tile) — kernel vs the
-fp64 oracle on the same bf16 inputs."""
+sizes, mixes of all five modes with random geometry, both storage orders —
+kernel vs the fp64 oracle on the same bf16 inputs.  Peaked cases (q x 8) put
+outputs near |o| = 4, where one bf16 ulp of the result is 0.031: the 2e-2
+bar then leaves ~4e-3 for the kernel's own error (rounded-P row sums keep
+it there)."""
 
 import numpy as np
 import pytest
@@ -48,12 +50,11 @@ def _random_case(rng):
     return lay, specs, d, B, qscale
 
 
-@pytest.mark.parametrize("cluster", ["4", "2"])
-def test_random_layers_vs_oracle(cluster, monkeypatch):
+@pytest.mark.parametrize("seed", [4, 2])
+def test_random_layers_vs_oracle(seed):
     import torch
 
-    monkeypatch.setenv("SVD_CLUSTER", cluster)
-    rng = np.random.default_rng(1234 + int(cluster))
+    rng = np.random.default_rng(1234 + seed)
     worst = 0.0
     done = 0
     for case in range(24):
@@ -67,7 +68,7 @@ def test_random_layers_vs_oracle(cluster, monkeypatch):
         q, k, v = O.bf16_round(q * np.float32(qscale)), O.bf16_round(k), O.bf16_round(v)
         want = O.fused_layer_attention(q, k, v, groups_o, og)
         layout = S.TokenLayout(*lay)
-        plan = S.LayerPlan.from_specs(specs, layout)  # fresh plan: picks up SVD_CLUSTER
+        plan = S.LayerPlan.from_specs(specs, layout)
         assert plan.info.n_work_items > 0
         tq, tk, tv = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v))
         if case % 2:  # [B, N, H, d] storage viewed as [B, H, N, d]
@@ -83,4 +84,4 @@ def test_random_layers_vs_oracle(cluster, monkeypatch):
         worst = max(worst, float(err.max()))
         done += 1
     assert done >= 18
-    print(f"cluster {cluster}: {done} cases, worst max-abs {worst:.3e}")
+    print(f"seed {seed}: {done} cases, worst max-abs {worst:.3e}")

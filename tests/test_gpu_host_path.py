@@ -40,3 +40,24 @@ def test_host_pipeline_unpinned_fp32():
     host = S.fused_layer_attention(q, k, v, S.group_heads(specs, g))
     dev = S.fused_layer_attention(q.cuda(), k.cuda(), v.cuda(), S.group_heads(specs, g)).cpu()
     assert torch.equal(host, dev)
+
+
+@pytest.mark.parametrize("d", [64, 40])
+def test_out_buffer_host_and_device(d):
+    """out= writes the caller's buffer in place (host pinned and device), same
+    bits as the allocating call."""
+    import torch
+
+    g = S.block_grid(S.TokenLayout(0, 8, 128, 64))
+    specs = [S.diagonal_spec(1), S.full_spec(), S.skip_spec()]
+    groups = S.group_heads(specs, g)
+    q, k, v = (torch.randn(1, 3, 1024, d).to(torch.bfloat16).pin_memory() for _ in range(3))
+    want = S.fused_layer_attention(q, k, v, groups)
+    hout = torch.full(q.shape, 7.0, dtype=torch.bfloat16).pin_memory()
+    got = S.fused_layer_attention(q, k, v, groups, out=hout)
+    assert got.data_ptr() == hout.data_ptr() and torch.equal(hout, want)
+    dout = torch.full(q.shape, 7.0, dtype=torch.bfloat16, device="cuda")
+    got = S.fused_layer_attention(q.cuda(), k.cuda(), v.cuda(), groups, out=dout)
+    assert got.data_ptr() == dout.data_ptr() and torch.equal(dout.cpu(), want)
+    with pytest.raises(S.ShapeError):
+        S.fused_layer_attention(q, k, v, groups, out=torch.empty(1, 3, 1024, d))
