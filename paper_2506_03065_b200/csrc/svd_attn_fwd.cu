@@ -39,26 +39,11 @@ constexpr int kThreads = 384;
 constexpr int kMaxPeers = 8;
 constexpr uint32_t kTmemCols = 512;
 
-#ifndef SVD_EARLY_S
-#define SVD_EARLY_S 0
-#endif
-#ifndef SVD_SPLIT_P
-#define SVD_SPLIT_P 1
-#endif
-#ifndef SVD_SPLIT_S
-#define SVD_SPLIT_S 0
-#endif
-#ifndef SVD_PINGPONG
-#define SVD_PINGPONG 0
-#endif
 // Row sums over the bf16-rounded P (the values the PV MMA consumes) rather
 // than the fp32 exps: numerator and denominator then see the same weights,
 // which removes the bf16 rounding of the dominant weight from peaked rows.
 #ifndef SVD_SUM_ROUNDED
 #define SVD_SUM_ROUNDED 1
-#endif
-#ifndef SVD_DYN_ISSUE
-#define SVD_DYN_ISSUE 0
 #endif
 
 template <int D>
@@ -69,16 +54,14 @@ struct KCfg {
   static constexpr int kTileBytes = 128 * D * 2;       // a Q tile or a KV tile
   static constexpr int kKSt = D == 128 ? 2 : 4;
   static constexpr int kVSt = D == 128 ? 2 : 4;
-  // d=64 leaves TMEM room for P next to S: S_X(j+1) is then issued as soon as
-  // the softmax has read S_X(j) ("early S"), decoupling the two pipelines.
-  // d=128 needs all 512 columns for S_A, S_B, O_A, O_B, so P_X aliases S_X and
-  // S_X(j+1) must follow PV_X(j).
-  static constexpr bool kEarlyS = D == 64 && SVD_EARLY_S;
+  // d=128 needs all 512 columns for S_A, S_B, O_A, O_B, so P_X aliases S_X
+  // (S_X(j+1) then follows PV_X(j) in the in-order tensor pipe); d=64 keeps P
+  // in its own columns.
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + 2 * kTileBytes;
   static constexpr int kOffV = kOffK + kKSt * kTileBytes;
   static constexpr int kOffBar = kOffV + kVSt * kTileBytes;
-  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p0[2] p1[2] o[2] sfree[2] pvdone[2]
+  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p0[2] p1[2] o[2]
   static constexpr int kBarQ = 0;
   static constexpr int kBarKF = 1;
   static constexpr int kBarKE = kBarKF + kKSt;
@@ -88,9 +71,7 @@ struct KCfg {
   static constexpr int kBarP0 = kBarS + 2;
   static constexpr int kBarP1 = kBarP0 + 2;
   static constexpr int kBarO = kBarP1 + 2;
-  static constexpr int kBarSFree = kBarO + 2;
-  static constexpr int kBarPVDone = kBarSFree + 2;
-  static constexpr int kNumBars = kBarPVDone + 2;
+  static constexpr int kNumBars = kBarO + 2;
   static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
   __device__ static constexpr uint32_t col_s(int x) { return x ? 128u : 0u; }
@@ -252,8 +233,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(bar(C::kBarP0 + x), 128);
       ptx::mbar_init(bar(C::kBarP1 + x), 128);
       ptx::mbar_init(bar(C::kBarO + x), 1);
-      ptx::mbar_init(bar(C::kBarSFree + x), 128);
-      ptx::mbar_init(bar(C::kBarPVDone + x), 1);
     }
     ptx::fence_barrier_init();
   }
@@ -324,24 +303,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_s = [&](int x, int ks) {
           const uint32_t qb = sb + C::kOffQ + x * C::kTileBytes;
           const uint32_t kb = sb + C::kOffK + ks * C::kTileBytes;
-#if SVD_SPLIT_S
-          constexpr uint32_t id_s64 = ptx::idesc_bf16(128, 64, false);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
-              ptx::mma_ss(tb + C::col_s(x) + hh * 64, ptx::sw128_desc(qb + off, 16, 1024),
-                          ptx::sw128_desc(kb + off + hh * 8192, 16, 1024), id_s64, kk > 0);
-            }
-#else
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * C::kSlabBytes + (kk & 3) * 32;
             ptx::mma_ss(tb + C::col_s(x), ptx::sw128_desc(qb + off, 16, 1024),
                         ptx::sw128_desc(kb + off, 16, 1024), id_s, kk > 0);
           }
-#endif
         };
         // O_X += P_X V_j, keys [64*half, 64*half + 64): four K=16 steps
         auto issue_pv_half = [&](int x, int vs, int half, bool acc) {
@@ -376,94 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_s(1, 0);
         ptx::mma_commit(bar(C::kBarS + 1));
         ptx::mma_commit(bar(C::kBarKE + 0));
-#if SVD_DYN_ISSUE
-        if constexpr (!C::kEarlyS) {
-          // Dynamic issue: poll both tiles and issue whichever PV half / next S
-          // is ready, instead of a fixed A-then-B order that blocks on one
-          // tile's P while the other tile's work is ready.  Per tile: phase 0
-          // = PV half 0 of step jx (needs V_jx + P0), 1 = PV half 1 (needs P1),
-          // 2 = S(jx+1) (needs K_{jx+1}).  A V / K slot is released when both
-          // tiles are past it; the rings bound the drift between tiles.
-          int jx[2] = {0, 0}, ph[2] = {0, 0};
-          int pv_done[2] = {0, 0}, s_done[2] = {0, 0};
-          bool fin[2] = {false, false};
-          int ve_next = 0, ke_next = 1;  // next step whose V / K slot to release
-          while (!(fin[0] && fin[1])) {
-#pragma unroll 1
-            for (int x = 0; x < 2; ++x) {
-              if (fin[x]) continue;
-              const int j = jx[x];
-              if (ph[x] == 0) {
-                if (!ptx::mbar_try_wait(bar(C::kBarVF + j % C::kVSt), (j / C::kVSt) & 1)) continue;
-                if (!ptx::mbar_try_wait(bar(C::kBarP0 + x), j & 1)) continue;
-                ptx::tc_fence_after();
-                issue_pv_half(x, j % C::kVSt, 0, j > 0);
-                ph[x] = 1;
-              }
-              if (ph[x] == 1) {
-                if (!ptx::mbar_try_wait(bar(C::kBarP1 + x), j & 1)) continue;
-                ptx::tc_fence_after();
-                issue_pv_half(x, j % C::kVSt, 1, j > 0);
-                pv_done[x] = j + 1;
-                if (min(pv_done[0], pv_done[1]) > ve_next) {
-                  ptx::mma_commit(bar(C::kBarVE + ve_next % C::kVSt));
-                  ++ve_next;
-                }
-                if (j + 1 == n_kv) {
-                  ptx::mma_commit(bar(C::kBarO + x));
-                  fin[x] = true;
-                  continue;
-                }
-                ph[x] = 2;
-              }
-              if (ph[x] == 2) {
-                const int ks1 = (j + 1) % C::kKSt;
-                if (!ptx::mbar_try_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1)) continue;
-                ptx::tc_fence_after();
-                issue_s(x, ks1);
-                ptx::mma_commit(bar(C::kBarS + x));
-                s_done[x] = j + 1;
-                if (min(s_done[0], s_done[1]) >= ke_next) {
-                  ptx::mma_commit(bar(C::kBarKE + ke_next % C::kKSt));
-                  ++ke_next;
-                }
-                jx[x] = j + 1;
-                ph[x] = 0;
-              }
-            }
-          }
-        }
-        for (int j = 0; j < n_kv && C::kEarlyS; ++j) {
-#else
         for (int j = 0; j < n_kv; ++j) {
-#endif
           asm volatile("" : "+r"(sb), "+r"(tb));
           const int vs = j % C::kVSt;
           const int ks1 = (j + 1) % C::kKSt;
           const bool more = j + 1 < n_kv;
-          if constexpr (C::kEarlyS) {
-            // next S tiles as soon as both the softmax has drained S and K_{j+1} landed
-            if (more) {
-              ptx::mbar_wait(bar(C::kBarKF + ks1), ((j + 1) / C::kKSt) & 1);
-              ptx::mbar_wait(bar(C::kBarSFree + 0), j & 1);
-              ptx::tc_fence_after();
-              issue_s(0, ks1);
-              ptx::mma_commit(bar(C::kBarS + 0));
-              ptx::mbar_wait(bar(C::kBarSFree + 1), j & 1);
-              ptx::tc_fence_after();
-              issue_s(1, ks1);
-              ptx::mma_commit(bar(C::kBarS + 1));
-              ptx::mma_commit(bar(C::kBarKE + ks1));
-            }
-            ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
-            issue_pv(0, vs, j);
-            ptx::mma_commit(bar(C::kBarPVDone + 0));
-            if (!more) ptx::mma_commit(bar(C::kBarO + 0));
-            issue_pv(1, vs, j);
-            ptx::mma_commit(bar(C::kBarPVDone + 1));
-            ptx::mma_commit(bar(C::kBarVE + vs));
-            if (!more) ptx::mma_commit(bar(C::kBarO + 1));
-          } else {
+          {
             ptx::mbar_wait(bar(C::kBarVF + vs), (j / C::kVSt) & 1);
             // tile A: PV (in two halves, as P arrives), then the next S
             issue_pv(0, vs, j);
@@ -544,10 +429,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   int tn = 0;
   const bool tr = (warp == 4 || warp == 8) && lane == 0;
 #endif
-  // Ping-pong: the two tiles' softmax warpgroups take turns on the exp phase
-  // (named barriers 2 = A's turn, 3 = B's turn), so one tile's MUFU work
-  // overlaps the other tile's MMAs instead of both contending for MUFU.
-  if (SVD_PINGPONG && x == 1) asm volatile("bar.arrive 2, 256;" ::: "memory");
+  // exps of one 32-key chunk of S against the reference max: packed bf16 P
+  // (pk) and the running row sums (over the rounded P, SVD_SUM_ROUNDED)
+  auto exp_chunk = [&](const float (&sv)[128], int c, const float2 nm, uint32_t (&pk)[16],
+                       float2 (&acc)[4]) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 xv = ptx::ffma2(make_float2(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]), sl2x2, nm);
+      float2 pv;
+      if ((i & 7) >= 8 - kEmuPairs<D>) {
+        pv = ptx::ex2_poly2(xv);
+      } else {
+        pv.x = ptx::ex2(xv.x);
+        pv.y = ptx::ex2(xv.y);
+      }
+      pk[i] = ptx::pack_bf16(pv.x, pv.y);
+      if (SVD_SUM_ROUNDED) ptx::acc_bf16x2(acc[i & 3], pk[i]);
+      else acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
+    }
+  };
+  const uint32_t tp = tmem + lane_off + C::col_p(x);
   for (int j = 0; j < n_kv; ++j) {
     const KvEntry e = e_next;
     if (j + 1 < n_kv) e_next = load_kv(kvp + j + 1);  // prefetch behind the S wait
@@ -566,16 +467,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tmem_ld32(ts + 64, *reinterpret_cast<float(*)[32]>(&s[64]));
     ptx::tmem_ld32(ts + 96, *reinterpret_cast<float(*)[32]>(&s[96]));
     ptx::tmem_wait_ld();
-    if constexpr (C::kEarlyS) {
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(bar(C::kBarSFree + x));  // S_X may now be overwritten by S_X(j+1)
-    }
 #ifdef SVD_TRACE
     if (tr) TRACE(x, tn, j, 3);  // S in registers
 #endif
     if (!(e.flags & kFlagAll)) apply_mask<FINE>(s, e, qslot, p, bits_row);
 
-    // row max: 8 independent FMNMX chains, then a short tree
+    // row max: 8 independent chains, then a short tree
     float mp[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) mp[t] = fmaxf(s[t], s[8 + t]);
@@ -586,13 +483,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                            fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
     const float m_new = fmaxf(m, mx * sl2);
-    if constexpr (C::kEarlyS) {
-      // O_X and the P_X buffer are still in use by PV_X(j-1) until it completes
-      if (j > 0) {
-        ptx::mbar_wait(bar(C::kBarPVDone + x), (j - 1) & 1);
-        ptx::tc_fence_after();
-      }
-    }
     // lazy rescale: keep a stale max unless it grew by more than 2^8
     const bool resc = m_new > m + 8.0f;
     if (__any_sync(0xffffffffu, resc)) {
@@ -616,55 +506,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const float mref = (m == -INFINITY) ? 0.f : m;
     const float2 nm = make_float2(-mref, -mref);
-    const uint32_t tp = tmem + lane_off + C::col_p(x);
 #ifdef SVD_TRACE
     if (tr) TRACE(x, tn, j, 4);  // max + rescale done
-#endif
-    if (SVD_PINGPONG) named_bar_sync(2 + x, 256);  // wait for my turn
-#ifdef SVD_TRACE
-    if (tr) TRACE(x, tn, j, 5);  // turn acquired
 #endif
     float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                      make_float2(0.f, 0.f)};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float2 xv = ptx::ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sl2x2, nm);
-        float2 pv;
-        if ((i & 7) >= 8 - kEmuPairs<D>) {
-          pv = ptx::ex2_poly2(xv);
-        } else {
-          pv.x = ptx::ex2(xv.x);
-          pv.y = ptx::ex2(xv.y);
-        }
-        pk[i] = ptx::pack_bf16(pv.x, pv.y);
-        if (SVD_SUM_ROUNDED) ptx::acc_bf16x2(acc[i & 3], pk[i]);
-        else acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
-      }
+      exp_chunk(s, c, nm, pk, acc);
       ptx::tmem_st16(tp + c * 16, pk);
-      if ((c == 1 && SVD_SPLIT_P) || c == 3) {
+      if (c == 1 || c == 3) {
         // hand P over in two 64-key halves: PV on the first half overlaps
         // the exps of the second
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        if (c == 1) ptx::mbar_arrive(bar(C::kBarP0 + x));
+        ptx::mbar_arrive(bar(c == 1 ? C::kBarP0 + x : C::kBarP1 + x));
 #ifdef SVD_TRACE
-        if (c == 1 && tr) TRACE(x, tn, j, 6);  // P half 0 handed over
+        if (tr) TRACE(x, tn, j, c == 1 ? 6 : 2);  // P half 0 / 1 handed over
 #endif
-        if (c == 3) {
-          if (!SVD_SPLIT_P) ptx::mbar_arrive(bar(C::kBarP0 + x));
-          ptx::mbar_arrive(bar(C::kBarP1 + x));
-          // hand the turn to the other tile (B skips its very last hand-over)
-          if (SVD_PINGPONG && (x == 0 || j + 1 < n_kv)) {
-            if (x == 0) asm volatile("bar.arrive 3, 256;" ::: "memory");
-            else asm volatile("bar.arrive 2, 256;" ::: "memory");
-          }
-#ifdef SVD_TRACE
-          if (tr) TRACE(x, tn, j, 2);
-#endif
-        }
       }
     }
     const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);

@@ -215,9 +215,10 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   p = ffma2(p, f, make_float2(0.6932609677f, 0.6932609677f));
   p = ffma2(p, f, make_float2(0.9999280572f, 0.9999280572f));
   float2 r;
-  // exponent insert as one IMAD: bits(t) * 2^23 == j << 23 (mod 2^32)
-  r.x = __int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x));
-  r.y = __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y));
+  // exponent insert: bits(t) << 23 == j << 23 (mod 2^32), added to bits(p) —
+  // one LEA on the ALU pipe (the FMA pipe already carries the polynomial)
+  r.x = __uint_as_float((__float_as_uint(t.x) << 23) + __float_as_uint(p.x));
+  r.y = __uint_as_float((__float_as_uint(t.y) << 23) + __float_as_uint(p.y));
   return r;
 }
 template <int N>
