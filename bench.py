@@ -211,6 +211,33 @@ def cpu_baseline(cfg, S, budget_s: float = 15.0) -> dict:
 
 
 # ----------------------------------------------------------------- GPU arm
+def library_dense(q, k, v, dev, reps: int = 3):
+    """Dense attention through torch SDPA on the same GPU and inputs — a
+    library baseline beside our own dense sm_100a launch (first backend that
+    runs: cuDNN, then flash, then memory-efficient)."""
+    import torch
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION):
+        try:
+            with sdpa_kernel([be]):
+                o = F.scaled_dot_product_attention(q, k, v)
+                torch.cuda.synchronize(dev)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(reps):
+                    o = F.scaled_dot_product_attention(q, k, v)
+                b.record()
+                torch.cuda.synchronize(dev)
+            del o
+            return {"backend": f"torch SDPA {be.name}", "ms": round(a.elapsed_time(b) / reps, 3)}
+        except Exception as exc:  # backend unavailable for this shape / build
+            last = f"{be.name}: {type(exc).__name__}"
+            torch.cuda.synchronize(dev)
+    return {"backend": None, "ms": None, "error": last}
+
+
 def init_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -335,6 +362,8 @@ def run_ours(args):
         b.record(stream)
         torch.cuda.synchronize(dev)
         dense_ms = a.elapsed_time(b) / reps
+        del dense_out
+    dense_lib = library_dense(q, k, v, dev) if (not args.no_dense and world == 1) else None
 
     if rank != 0:
         return
@@ -373,6 +402,9 @@ def run_ours(args):
         "kernel_ms": round(kms, 4),
         "dense_ms": round(dense_ms, 3) if dense_ms else None,
         "speedup_vs_dense": round(dense_ms / ms, 3) if dense_ms else None,
+        "dense_library": dense_lib,
+        "speedup_vs_dense_library": (round(dense_lib["ms"] / ms, 3)
+                                     if dense_lib and dense_lib.get("ms") else None),
         "roofline": {
             "bound": "tensor",
             "achieved": round(achieved, 2),

@@ -51,6 +51,8 @@ for cta in range(8):
         per = np.median([(ready[j + 1] - ready[j]) & 0xFFFFFFFF for j in js])
         r[f"tile{x}"] = {"softmax_active": float(act), "wait_S": float(wait), "period": float(per)}
         ph = {c: times(x, c) for c in (3, 4, 5, 6)}
+        if not ph[5]:  # no ping-pong turn event: the exp phase starts at event 4
+            ph[5] = ph[4]
         def med(a, b):
             v = [(b[j] - a[j]) & 0xFFFFFFFF for j in js if j in a and j in b]
             return float(np.median(v)) if v else None
