@@ -16,6 +16,9 @@
  *   attention.py:57-98  sparse_attention(q,k,v,mask)   svd_plan_create_from_masks + svd_attn_fwd
  *   attention.py:101-105 full_mask_attention(...)      svd_plan_create (FULL spec) + svd_attn_fwd
  *   attention.py:51-54  skip_attention(...)            svd_plan_create (SKIP spec) + svd_attn_fwd
+ *   model.py:352-355    _layernorm (layer_qkv / layer_finish)   svd_layernorm
+ *   model.py:169-195    rope(q), rope(k) (layer_qkv)            svd_rope_table + svd_rope_apply
+ *   model.py:357-359    _gelu (layer_finish MLP)                svd_gelu
  *
  * Conventions
  *  - Every function returns an svd_status; on failure a message is available
@@ -196,6 +199,29 @@ int svd_head_sqdiff(const void* a, const void* b, const int64_t* a_strides,
 int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, int64_t n_rows,
                     const void* packed, int64_t packed_row_stride, void* o,
                     const int64_t* o_strides, int32_t head_dim, void* stream);
+
+/* ---- steps either side of the operator (model.py:372-402) ------------------
+ * The projections are plain GEMMs (cuBLAS); these are the streaming passes
+ * between them.  All pointers are device pointers, 16-byte aligned. */
+
+/* LayerNorm without affine over rows of `dim` fp32 values (model.py:352-355),
+ * bf16 output y.  resid != NULL fuses the residual add first: x_out = x +
+ * resid (fp32, may alias x) and y = LN(x_out).  dim % 4 == 0. */
+int svd_layernorm(const float* x, const float* resid, float* x_out, void* y, int64_t rows,
+                  int32_t dim, float eps, void* stream);
+
+/* RoPE table (model.py:169-195): table[n][c] = (cos, sin)(n * base^(-2c/d)),
+ * float2[n_tokens][head_dim / 2], computed in fp64. */
+int svd_rope_table(void* table, int64_t n_tokens, int32_t head_dim, double base, void* stream);
+
+/* RoPE in place on the q block (columns [0, H*d)) and the k block (columns
+ * [k_off, k_off + H*d)) of a bf16 [rows = B*N, ld] projection output; row r
+ * is token r % n_tokens.  head_dim % 8 == 0, ld and k_off multiples of 8. */
+int svd_rope_apply(void* qkv, int64_t rows, int64_t ld, int64_t k_off, int64_t n_tokens,
+                   int32_t heads, int32_t head_dim, const void* table, void* stream);
+
+/* Exact GELU in place on `count` bf16 values (model.py:357-359); count % 8 == 0. */
+int svd_gelu(void* u, int64_t count, void* stream);
 
 #ifdef __cplusplus
 }

@@ -327,3 +327,95 @@ def active_pairs(active: np.ndarray, bounds: np.ndarray) -> float:
     """Sum over active (qb, kb) of |qb|*|kb| (FLOPs = 4*d*this, costmodel.py:26-32)."""
     sizes = np.diff(bounds).astype(np.float64)
     return float(sizes @ active.astype(np.float64) @ sizes)
+
+
+# ------------------------------------------------------------------ the block around the operator
+# (SURVEY §8 row f4: layer_qkv / layer_finish, the steps either side of the
+# attention call in model.layer_forward, model.py:405-420)
+ROPE_BASE = 10000.0  # model.py:39
+
+
+def layer_weights(seed: int, layer: int, heads: int, head_dim: int, ffn_mult: int = 4) -> dict:
+    """wq, wk, wv, wo, w1, w2 of one layer, drawn like build_model
+    (model.py:312-324: make_rng(seed, 1, layer, slot), N(0,1)/sqrt(rows), fp32)."""
+    dim = heads * head_dim
+    hidden = ffn_mult * dim
+    shapes = {"wq": (dim, dim), "wk": (dim, dim), "wv": (dim, dim), "wo": (dim, dim),
+              "w1": (dim, hidden), "w2": (hidden, dim)}
+    out = {}
+    for slot, (name, (rows, cols)) in enumerate(shapes.items()):
+        rng = make_rng(seed, 1, layer, slot)
+        out[name] = (rng.standard_normal((rows, cols)) / np.sqrt(rows)).astype(np.float32)
+    return out
+
+
+def zero_redundant_heads(w: dict, heads, head_dim: int) -> dict:
+    """A "redundant" plant zeroes the head's value and output paths
+    (model.py:346-348)."""
+    for h in heads:
+        w["wv"][:, h * head_dim:(h + 1) * head_dim] = 0.0
+        w["wo"][h * head_dim:(h + 1) * head_dim, :] = 0.0
+    return w
+
+
+def layernorm(x64: np.ndarray) -> np.ndarray:
+    """model.py:352-355 (no affine, eps 1e-5, biased variance, fp64)."""
+    mean = x64.mean(axis=-1, keepdims=True)
+    var = x64.var(axis=-1, keepdims=True)
+    return (x64 - mean) / np.sqrt(var + 1e-5)
+
+
+def gelu(x64: np.ndarray) -> np.ndarray:
+    """model.py:357-359, exact erf GELU."""
+    from math import erf, sqrt
+
+    return 0.5 * x64 * (1.0 + np.vectorize(erf)(x64 / sqrt(2.0)))
+
+
+def rope(x: np.ndarray) -> np.ndarray:
+    """model.py:169-195: pair (2c, 2c+1) rotated by n * base^(-2c/d), fp64, fp32 out."""
+    d, n = x.shape[-1], x.shape[-2]
+    theta = ROPE_BASE ** (-2.0 * np.arange(d // 2) / d)
+    ang = np.arange(n, dtype=np.float64)[:, None] * theta[None, :]
+    cos, sin = np.cos(ang), np.sin(ang)
+    x64 = x.astype(np.float64)
+    even, odd = x64[..., 0::2], x64[..., 1::2]
+    out = np.empty_like(x64)
+    out[..., 0::2] = even * cos - odd * sin
+    out[..., 1::2] = even * sin + odd * cos
+    return out.astype(np.float32)
+
+
+def split_heads(x: np.ndarray, heads: int) -> np.ndarray:
+    """model.py:362-364: [B, N, D] -> [B, H, N, d]."""
+    b, n, dim = x.shape
+    return x.reshape(b, n, heads, dim // heads).transpose(0, 2, 1, 3)
+
+
+def merge_heads(x: np.ndarray) -> np.ndarray:
+    """model.py:367-369: [B, H, N, d] -> [B, N, D]."""
+    b, h, n, d = x.shape
+    return x.transpose(0, 2, 1, 3).reshape(b, n, h * d)
+
+
+def layer_qkv(w: dict, x: np.ndarray, heads: int, planted_q=None, planted_k=None):
+    """model.py:372-391: LN -> fp64 projections -> fp32 heads -> RoPE(q, k);
+    planted heads' q/k replaced by their stored codes after RoPE."""
+    h64 = layernorm(np.asarray(x, dtype=np.float64))
+    q = split_heads((h64 @ w["wq"].astype(np.float64)).astype(np.float32), heads)
+    k = split_heads((h64 @ w["wk"].astype(np.float64)).astype(np.float32), heads)
+    v = split_heads((h64 @ w["wv"].astype(np.float64)).astype(np.float32), heads)
+    q, k = rope(q), rope(k)
+    for head, code in (planted_q or {}).items():
+        q[:, head] = code[None]
+    for head, code in (planted_k or {}).items():
+        k[:, head] = code[None]
+    return q, k, v
+
+
+def layer_finish(w: dict, x: np.ndarray, attn_out: np.ndarray) -> np.ndarray:
+    """model.py:394-402: x + merge(attn) Wo, then + GELU(LN(.) W1) W2 (fp64, fp32 out)."""
+    x64 = np.asarray(x, dtype=np.float64)
+    a = x64 + merge_heads(np.asarray(attn_out, dtype=np.float64)) @ w["wo"].astype(np.float64)
+    f = a + gelu(layernorm(a) @ w["w1"].astype(np.float64)) @ w["w2"].astype(np.float64)
+    return f.astype(np.float32)

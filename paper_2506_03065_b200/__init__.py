@@ -58,6 +58,7 @@ from .search import (
     select_mode,
     sparsity_table,
 )
+from .layer import DeviceModel, layer_finish, layer_forward, layer_qkv
 from .costmodel import B200LatencyModel, attention_flops, attention_latency_share, layer_linear_flops
 
 __all__ = [name for name in dir() if not name.startswith("_")]

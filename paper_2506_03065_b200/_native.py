@@ -121,6 +121,12 @@ SIGNATURES = {
         c_int,
         [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, POINTER(c_int64), c_int32, c_void_p],
     ),
+    "svd_layernorm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, ctypes.c_float,
+                              c_void_p]),
+    "svd_rope_table": (c_int, [c_void_p, c_int64, c_int32, c_double, c_void_p]),
+    "svd_rope_apply": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p,
+                               c_void_p]),
+    "svd_gelu": (c_int, [c_void_p, c_int64, c_void_p]),
 }
 
 _lib = None

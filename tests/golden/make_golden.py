@@ -267,8 +267,48 @@ def attn_fixtures():
     np.savez_compressed(OUT / "golden_attn.npz", **data)
 
 
+def layer_fixtures():
+    """A planted 2-layer toy model (model.py:307-349): layer 1's layer_qkv,
+    the fused attention under a per-head assignment, layer_finish and
+    layer_forward (model.py:372-420), all from the reference.  Weights are
+    not stored (tests redraw them with the oracle and check these digests)."""
+    import hashlib
+
+    from svdit import model as M
+
+    layout = TokenLayout(64, 2, 128, 64)
+    plant = {(1, 0): M.PlantDirective("diagonal"), (1, 1): M.PlantDirective("vertical_stripe", 2),
+             (1, 2): M.PlantDirective("redundant"), (1, 3): M.PlantDirective("uniform")}
+    spec = M.ModelSpec(layers=2, heads=4, head_dim=32, layout=layout, timesteps=2, seed=11, plant=plant)
+    model = M.build_model(spec)
+    lw = model.layers[1]
+    x = make_rng(5, 77).standard_normal((1, layout.total_tokens, spec.hidden_dim)).astype(np.float32)
+    q, k, v = M.layer_qkv(model, 1, x)
+    stripes = model.planted_stripes[(1, 1)]
+    assignment = [diagonal_spec(1), vertical_stripe_spec(stripes=stripes), skip_spec(), full_spec()]
+    attn = fused_layer_attention(q, k, v, group_heads(assignment, model.grid))
+    data = {
+        "layout": np.array([64, 2, 128, 64], dtype=np.int64),
+        "meta": np.array([2, 4, 32, 11, 1], dtype=np.int64),  # layers, heads, head_dim, seed, layer
+        "stripes": np.array(stripes, dtype=np.int64),
+        "x": x, "q": q, "k": k, "v": v, "attn": attn,
+        "finish": M.layer_finish(model, 1, x, attn),
+        "forward": M.layer_forward(model, 1, x, assignment),
+        "planted_heads": np.array(sorted(lw.planted_q), dtype=np.int64),
+        "redundant_heads": np.array([2], dtype=np.int64),
+    }
+    for h in sorted(lw.planted_q):
+        data[f"planted_q{h}"] = lw.planted_q[h]
+        data[f"planted_k{h}"] = lw.planted_k[h]
+    for slot in ("wq", "wk", "wv", "wo", "w1", "w2"):
+        digest = hashlib.sha256(np.ascontiguousarray(getattr(lw, slot)).tobytes()).hexdigest()
+        data[f"sha_{slot}"] = np.frombuffer(bytes.fromhex(digest), dtype=np.uint8)
+    np.savez_compressed(OUT / "golden_layer.npz", **data)
+
+
 if __name__ == "__main__":
     plan_fixtures()
     attn_fixtures()
-    for f in ("golden_plan.npz", "golden_attn.npz"):
+    layer_fixtures()
+    for f in ("golden_plan.npz", "golden_attn.npz", "golden_layer.npz"):
         print(f, (OUT / f).stat().st_size, "bytes")

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import svdit_oracle as O
-from conftest import decode_spec, unpack_mask
+from conftest import GOLDEN, decode_spec, unpack_mask
 
 
 def test_rng_and_random_qkv(golden_attn):
@@ -137,3 +137,35 @@ def test_block_key_mass(golden_attn):
         got = O.block_key_mass(q, k, g)
         np.testing.assert_allclose(got, golden_attn[f"bkm{bi}_out"], rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=1e-9)
+
+
+# ---------------------------------------------------------------- the block around the operator (f4)
+def _golden_layer():
+    import hashlib
+
+    g = np.load(GOLDEN / "golden_layer.npz")
+    layers, heads, d, seed, li = (int(v) for v in g["meta"])
+    w = O.zero_redundant_heads(O.layer_weights(seed, li, heads, d), g["redundant_heads"], d)
+    for slot, arr in w.items():
+        assert hashlib.sha256(np.ascontiguousarray(arr).tobytes()).digest() == g[f"sha_{slot}"].tobytes(), slot
+    pq = {int(h): g[f"planted_q{h}"] for h in g["planted_heads"]}
+    pk = {int(h): g[f"planted_k{h}"] for h in g["planted_heads"]}
+    return g, w, heads, pq, pk
+
+
+def test_oracle_layer_weights_match_reference_digests():
+    _golden_layer()
+
+
+def test_oracle_layer_qkv_matches_reference():
+    g, w, heads, pq, pk = _golden_layer()
+    q, k, v = O.layer_qkv(w, g["x"], heads, pq, pk)
+    for name, got in (("q", q), ("k", k), ("v", v)):
+        np.testing.assert_allclose(got, g[name], rtol=0, atol=1e-6, err_msg=name)
+
+
+def test_oracle_layer_finish_matches_reference():
+    g, w, *_ = _golden_layer()
+    np.testing.assert_allclose(O.layer_finish(w, g["x"], g["attn"]), g["finish"], rtol=0, atol=1e-5)
+    # layer_forward = layer_finish(layer_qkv -> fused attention)
+    np.testing.assert_array_equal(g["finish"], g["forward"])
