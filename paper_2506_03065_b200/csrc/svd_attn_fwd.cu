@@ -42,9 +42,6 @@ constexpr uint32_t kTmemCols = 512;
 // Row sums over the bf16-rounded P (the values the PV MMA consumes) rather
 // than the fp32 exps: numerator and denominator then see the same weights,
 // which removes the bf16 rounding of the dominant weight from peaked rows.
-#ifndef SVD_P_CHUNKS
-#define SVD_P_CHUNKS 4
-#endif
 #ifndef SVD_SUM_ROUNDED
 #define SVD_SUM_ROUNDED 1
 #endif
@@ -64,17 +61,16 @@ struct KCfg {
   static constexpr int kOffK = kOffQ + 2 * kTileBytes;
   static constexpr int kOffV = kOffK + kKSt * kTileBytes;
   static constexpr int kOffBar = kOffV + kVSt * kTileBytes;
-  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p[2][kPChunks] o[2]
+  // barriers: q | kfull[K] kempty[K] | vfull[V] vempty[V] | s[2] p0[2] p1[2] o[2]
   static constexpr int kBarQ = 0;
   static constexpr int kBarKF = 1;
   static constexpr int kBarKE = kBarKF + kKSt;
   static constexpr int kBarVF = kBarKE + kKSt;
   static constexpr int kBarVE = kBarVF + kVSt;
   static constexpr int kBarS = kBarVE + kVSt;
-  // P is handed to the PV MMAs in kPChunks slices of 128 / kPChunks keys
-  static constexpr int kPChunks = SVD_P_CHUNKS;
-  static constexpr int kBarP = kBarS + 2;  // [x * kPChunks + c]
-  static constexpr int kBarO = kBarP + 2 * kPChunks;
+  static constexpr int kBarP0 = kBarS + 2;
+  static constexpr int kBarP1 = kBarP0 + 2;
+  static constexpr int kBarO = kBarP1 + 2;
   static constexpr int kNumBars = kBarO + 2;
   static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
@@ -234,7 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(bar(C::kBarS + x), 1);
-      for (int c = 0; c < C::kPChunks; ++c) ptx::mbar_init(bar(C::kBarP + x * C::kPChunks + c), 128);
+      ptx::mbar_init(bar(C::kBarP0 + x), 128);
+      ptx::mbar_init(bar(C::kBarP1 + x), 128);
       ptx::mbar_init(bar(C::kBarO + x), 1);
     }
     ptx::fence_barrier_init();
@@ -330,13 +327,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_s(tb + C::col_s(x), qlo + off, klo + off, hi, id_s, kk > 0);
           }
         };
-        // O_X += P_X V_j on the keys of P slice c: 8 / kPChunks K=16 steps
-        constexpr int kStepsPerChunk = 8 / C::kPChunks;
-        auto issue_pv_chunk = [&](int x, int vs, int c, bool acc) {
+        // O_X += P_X V_j, keys [64*half, 64*half + 64): four K=16 steps
+        auto issue_pv_half = [&](int x, int vs, int half, bool acc) {
           const uint32_t vlo = ptx::sw128_lo(sb + C::kOffV + vs * C::kTileBytes, C::kSlabBytes);
 #pragma unroll
-          for (int k4 = 0; k4 < kStepsPerChunk; ++k4) {
-            const int kk = c * kStepsPerChunk + k4;
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = half * 4 + k4;
             mma_t(tb + C::col_o(x), tb + C::col_p(x) + kk * 8, vlo + ((kk * 2048) >> 4), hi, id_pv,
                   (acc || kk > 0) ? 1u : 0u);
           }
@@ -345,14 +341,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         (void)tn;
         auto issue_pv = [&](int x, int vs, int j) {
           TRACE(2, tn, j, 30 + x);
-#pragma unroll
-          for (int c = 0; c < C::kPChunks; ++c) {
-            ptx::mbar_wait(bar(C::kBarP + x * C::kPChunks + c), j & 1);
-            if (c == 0) TRACE(2, tn, j, 40 + x);
-            if (c == C::kPChunks - 1) TRACE(2, tn, j, 50 + x);
-            ptx::tc_fence_after();
-            issue_pv_chunk(x, vs, c, j > 0);
-          }
+          ptx::mbar_wait(bar(C::kBarP0 + x), j & 1);
+          TRACE(2, tn, j, 40 + x);
+          ptx::tc_fence_after();
+          issue_pv_half(x, vs, 0, j > 0);
+          ptx::mbar_wait(bar(C::kBarP1 + x), j & 1);
+          TRACE(2, tn, j, 50 + x);
+          ptx::tc_fence_after();
+          issue_pv_half(x, vs, 1, j > 0);
           TRACE(2, tn, j, 10 + x);
         };
         ptx::mbar_wait(bar(C::kBarQ), 0);
@@ -536,14 +532,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[16];
       exp_chunk(s, c, nm, pk, acc);
       ptx::tmem_st16(tp + c * 16, pk);
-      constexpr int kPer = 4 / C::kPChunks;  // 32-key chunks per P slice
-      if ((c + 1) % kPer == 0) {
-        // hand P over slice by slice: PV on the finished keys overlaps the
-        // exps of the rest, and only the last slice's PV sits between this
-        // softmax and the next S on the tensor pipe
+      if (c == 1 || c == 3) {
+        // hand P over in two 64-key halves: PV on the first half overlaps
+        // the exps of the second
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(bar(C::kBarP + x * C::kPChunks + c / kPer));
+        ptx::mbar_arrive(bar(c == 1 ? C::kBarP0 + x : C::kBarP1 + x));
 #ifdef SVD_TRACE
         if (tr) TRACE(x, tn, j, c == 1 ? 6 : 2);  // P half 0 / 1 handed over
 #endif
