@@ -100,6 +100,8 @@ typedef struct svd_plan_info {
                                /* active FLOPs = 4 * d * active_pairs          */
                                /* (costmodel.py:26-32 convention)              */
   double  dense_pairs;         /* N^2 * H                                      */
+  int32_t n_split_groups;      /* split-KV items (shard views), else 0         */
+  int32_t max_split_parts;     /* parts of the most-split item (1 if none)     */
 } svd_plan_info;
 
 /* Thread-local text of the last error (never NULL). */
@@ -146,6 +148,12 @@ int svd_plan_group_csr(const svd_plan* plan, int32_t g, int64_t* row_ptr, int64_
  * a packed [rows, d] buffer; svd_plan_shard_rows() reports the row count and
  * the (head, token) of every packed row (for the all-gather unpack). */
 int svd_plan_shard(const svd_plan* plan, int32_t world, int32_t rank, svd_plan** shard);
+/* As svd_plan_shard, with the shard's long items split along their KV list
+ * (split-KV, merged in the kernel) so no item exceeds max_item_tiles 128-key
+ * tiles: 0 = an eighth of the shard's mean per-SM load on n_sms SMs (what
+ * svd_plan_shard does with n_sms = 148), < 0 = never split. */
+int svd_plan_shard_sm(const svd_plan* plan, int32_t world, int32_t rank, int32_t n_sms,
+                      int32_t max_item_tiles, svd_plan** shard);
 int svd_plan_shard_rows(const svd_plan* shard, int64_t* n_rows, int32_t* row_head,
                         int32_t* row_token);
 

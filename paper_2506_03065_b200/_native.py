@@ -72,6 +72,8 @@ class SvdPlanInfo(ctypes.Structure):
         ("computed_tiles", c_int64),
         ("active_pairs", c_double),
         ("dense_pairs", c_double),
+        ("n_split_groups", c_int32),
+        ("max_split_parts", c_int32),
     ]
 
 
@@ -96,6 +98,7 @@ SIGNATURES = {
     "svd_plan_group_csr": (c_int, [c_void_p, c_int32, c_void_p, c_void_p]),
     "svd_plan_schedule": (c_int, [c_void_p, c_void_p, c_void_p]),
     "svd_plan_shard": (c_int, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),
+    "svd_plan_shard_sm": (c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, POINTER(c_void_p)]),
     "svd_plan_shard_rows": (c_int, [c_void_p, POINTER(c_int64), c_void_p, c_void_p]),
     "svd_attn_fwd": (
         c_int,

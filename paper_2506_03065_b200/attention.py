@@ -146,9 +146,16 @@ class LayerPlan:
         return 4.0 * head_dim * self.info.dense_pairs
 
     # -- multi-GPU
-    def shard(self, world: int, rank: int) -> "LayerPlan":
+    def shard(self, world: int, rank: int, n_sms: int | None = None, max_item_tiles: int = 0) -> "LayerPlan":
+        """This rank's share of the work items (LPT over ranks), with items
+        longer than max_item_tiles KV tiles split along the KV list and merged
+        in the kernel (0: an eighth of the shard's mean per-SM load on n_sms
+        SMs — the current device's count, 148 on B200; < 0: never split)."""
+        if n_sms is None:
+            n_sms = _device_sm_count()
         out = nat.c_void_p()
-        nat.check(nat.lib().svd_plan_shard(self._handle, world, rank, nat.ctypes.byref(out)))
+        nat.check(nat.lib().svd_plan_shard_sm(self._handle, world, rank, int(n_sms), int(max_item_tiles),
+                                              nat.ctypes.byref(out)))
         return LayerPlan(out.value, self.layout, self.n_heads, sharded=True)
 
     def shard_rows(self) -> tuple[np.ndarray, np.ndarray]:
@@ -185,6 +192,17 @@ class LayerPlan:
             self._handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
             nat.c_void_p(v.data_ptr()), nat.c_void_p(out.data_ptr()), st[0], st[1], st[2], ost,
             int(batch), hd, int(d_t), 0, nat.c_void_p(stream.cuda_stream)))
+
+
+def _device_sm_count() -> int:
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return int(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)
+    except Exception:  # no CUDA runtime: plan for a B200
+        pass
+    return 148
 
 
 _PLAN_CACHE: "OrderedDict[tuple, LayerPlan]" = OrderedDict()

@@ -37,6 +37,7 @@ namespace svd {
 
 constexpr int kThreads = 384;
 constexpr int kMaxPeers = 8;
+constexpr int kMaxSplitPartsDev = 8;  // == kMaxSplitParts of the plan builder
 constexpr uint32_t kTmemCols = 512;
 
 // Row sums over the bf16-rounded P (the values the PV MMA consumes) rather
@@ -99,6 +100,12 @@ struct FwdParams {
   // with the same [B, H, N, D] strides; `o` / `packed` are then unused.
   int n_peers;
   __nv_bfloat16* peer_o[kMaxPeers];
+  // split-KV merge (items with split_group >= 0): partial O rows [group][part][256][128]
+  // fp32, then (m, l) [group][part][256][2]; one ticket per group
+  float* split_o;
+  float* split_ml;
+  int* split_tickets;
+  int max_split_parts;
 };
 
 // Store one 16-byte chunk of an output row: to o + off, or to every peer.
@@ -551,21 +558,99 @@ __global__ void __launch_bounds__(kThreads, 1)
   // epilogue: O / l -> bf16 rows
   ptx::mbar_wait(bar(C::kBarO + x), 0);
   ptx::tc_fence_after();
-  const float inv = l > 0.f ? 1.0f / l : 0.f;
   const uint32_t to = tmem + lane_off + C::col_o(x);
+  if (itp->split_group < 0) {
+    const float inv = l > 0.f ? 1.0f / l : 0.f;
 #pragma unroll
-  for (int c = 0; c < D / 32; ++c) {
-    float ov[32];
-    ptx::tmem_ld32(to + c * 32, ov);
-    ptx::tmem_wait_ld();
-    uint32_t pk[16];
+    for (int c = 0; c < D / 32; ++c) {
+      float ov[32];
+      ptx::tmem_ld32(to + c * 32, ov);
+      ptx::tmem_wait_ld();
+      uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
-    if (row_valid) {
+      for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
+      if (row_valid) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        store_row16(p, orow + c * 32 + i * 8,
-                    make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+        for (int i = 0; i < 4; ++i)
+          store_row16(p, orow + c * 32 + i * 8,
+                      make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+      }
+    }
+  } else {
+    // split-KV part: publish the partial state (O relative to m, l), then the
+    // part that finishes last merges all parts (flash-decoding style):
+    // M = max m_p, O = sum 2^(m_p - M) O_p, L = sum 2^(m_p - M) l_p.
+    const int sg = itp->split_group, parts = itp->split_parts;
+    const int64_t slot = (int64_t(sg) * p.max_split_parts + itp->split_part) * 256 + x * 128 + row;
+    float* po = p.split_o + slot * 128;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      float ov[32];
+      ptx::tmem_ld32(to + c * 32, ov);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        __stcg(reinterpret_cast<float4*>(po + c * 32) + i,
+               make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]));
+    }
+    __stcg(reinterpret_cast<float2*>(p.split_ml) + slot, make_float2(m, l));
+    __threadfence();
+    volatile int* flag = reinterpret_cast<volatile int*>(base_ptr + C::kOffTmemSlot + 4);
+    named_bar_sync(2, 256);
+    if (threadIdx.x == 128) *flag = (atomicAdd(p.split_tickets + sg, 1) == parts - 1) ? 1 : 0;
+    named_bar_sync(2, 256);
+    if (*flag) {
+      __threadfence();
+      const int64_t row0 = int64_t(sg) * p.max_split_parts * 256 + x * 128 + row;
+      float mp[kMaxSplitPartsDev], wp[kMaxSplitPartsDev];
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < kMaxSplitPartsDev; ++q) {
+        mp[q] = -INFINITY;
+        if (q < parts) {
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.split_ml) + row0 + q * 256);
+          mp[q] = ml.x;
+          wp[q] = ml.y;  // l_p for now
+          M = fmaxf(M, ml.x);
+        }
+      }
+      float L = 0.f;
+#pragma unroll
+      for (int q = 0; q < kMaxSplitPartsDev; ++q) {
+        const float w = (q < parts && mp[q] != -INFINITY) ? ptx::ex2(mp[q] - M) : 0.f;
+        if (q < parts) L += w * wp[q];
+        wp[q] = w;
+      }
+      const float inv = L > 0.f ? 1.0f / L : 0.f;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int q = 0; q < kMaxSplitPartsDev; ++q) {
+          if (q >= parts) break;
+          const float4* src = reinterpret_cast<const float4*>(p.split_o + (row0 + q * 256) * 128 + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 v = __ldcg(src + i);
+            acc[4 * i] += wp[q] * v.x;
+            acc[4 * i + 1] += wp[q] * v.y;
+            acc[4 * i + 2] += wp[q] * v.z;
+            acc[4 * i + 3] += wp[q] * v.w;
+          }
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(acc[2 * i] * inv, acc[2 * i + 1] * inv);
+        if (row_valid) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            store_row16(p, orow + c * 32 + i * 8,
+                        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+        }
+      }
+      if (threadIdx.x == 128) p.split_tickets[sg] = 0;  // ready for the next launch
     }
   }
   if (p.n_peers > 0) __threadfence_system();  // peer rows visible before the kernel retires
@@ -690,6 +775,12 @@ static int ensure_device_tables(const svd_plan* P, DeviceTables** out) {
                   P->fine_bits.size() * 4)) != cudaSuccess ||
       (e = upload(&t.bit_off, P->fine_bit_off.data(), P->fine_bit_off.size() * 8)) != cudaSuccess)
     return cuda_fail(e, "plan upload");
+  if (P->n_split_groups > 0) {
+    const size_t parts = size_t(P->n_split_groups) * size_t(P->max_split_parts) * 256;
+    if ((e = upload(&t.split_scratch, nullptr, parts * (128 + 2) * sizeof(float))) != cudaSuccess ||
+        (e = upload(&t.split_tickets, nullptr, size_t(P->n_split_groups) * sizeof(int32_t))) != cudaSuccess)
+      return cuda_fail(e, "split-KV scratch");
+  }
   t.n_items = int64_t(P->items.size());
   auto res = P->dev.emplace(dev, t);
   *out = &res.first->second;
@@ -706,6 +797,8 @@ void release_device_tables(const svd_plan* P) {
     cudaFree(kv.second.kv);
     cudaFree(kv.second.bits);
     cudaFree(kv.second.bit_off);
+    cudaFree(kv.second.split_scratch);
+    cudaFree(kv.second.split_tickets);
   }
   P->dev.clear();
   cudaSetDevice(cur);
@@ -751,6 +844,13 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   prm.packed = P->sharded ? 1 : 0;
   prm.scale_log2 = float(1.4426950408889634 / std::sqrt(double(head_dim)));
   prm.n_peers = n_peers;
+  if (P->n_split_groups > 0) {
+    const size_t rows = size_t(P->n_split_groups) * size_t(P->max_split_parts) * 256;
+    prm.split_o = static_cast<float*>(T->split_scratch);
+    prm.split_ml = prm.split_o + rows * 128;
+    prm.split_tickets = static_cast<int*>(T->split_tickets);
+    prm.max_split_parts = P->max_split_parts;
+  }
   for (int r = 0; r < n_peers; ++r) prm.peer_o[r] = static_cast<__nv_bfloat16*>(peers[r]);
   if (T->n_items == 0) return SVD_OK;
   dim3 grid(unsigned(T->n_items), unsigned(batch));

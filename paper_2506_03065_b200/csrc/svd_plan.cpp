@@ -11,6 +11,8 @@
 // query segments clustered four to a CTA, each cluster with one ascending
 // list of 128-key tiles (pairs of key segments) plus per-tile activity bits.
 #include <algorithm>
+#include <functional>
+#include <queue>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -358,6 +360,9 @@ static void finalize_plan(svd_plan* P) {
         it.kv_count = grp.qgroup_kv_count[qi];
         for (int k = 0; k < kSlotsPerItem; ++k) it.qseg[k] = grp.qgroups[qi][k];
         it.out_base = -1;
+        it.split_group = -1;
+        it.split_part = 0;
+        it.split_parts = 1;
         P->items.push_back(it);
       }
     }
@@ -367,6 +372,42 @@ static void finalize_plan(svd_plan* P) {
                    [](const WorkItem& a, const WorkItem& b) { return a.kv_count > b.kv_count; });
   P->computed_tiles = 0;
   for (const auto& it : P->items) P->computed_tiles += 2 * int64_t(it.kv_count);
+}
+
+// Split-KV for SM balance inside a shard: an item whose KV list exceeds
+// `cap` tiles is cut into ceil(kv / cap) contiguous parts (at most
+// kMaxSplitParts); the kernel merges the parts' partial softmax states in
+// the epilogue of whichever part finishes last.  Re-sorted heaviest-first.
+constexpr int kMaxSplitParts = 8;
+constexpr double kItemOverhead = 4.0;  // per-CTA fixed cost, in KV tile steps
+static void split_items(svd_plan* S, int64_t cap) {
+  S->n_split_groups = 0;
+  S->max_split_parts = 1;
+  if (cap <= 0) return;
+  std::vector<WorkItem> out;
+  out.reserve(S->items.size());
+  for (const auto& it : S->items) {
+    const int64_t parts = std::min<int64_t>(kMaxSplitParts, (int64_t(it.kv_count) + cap - 1) / cap);
+    if (it.kv_count <= cap || parts < 2) {
+      out.push_back(it);
+      continue;
+    }
+    const int32_t gid = S->n_split_groups++;
+    S->max_split_parts = std::max<int32_t>(S->max_split_parts, int32_t(parts));
+    for (int64_t p = 0; p < parts; ++p) {
+      WorkItem w = it;
+      const int64_t b0 = int64_t(it.kv_count) * p / parts, b1 = int64_t(it.kv_count) * (p + 1) / parts;
+      w.kv_begin = it.kv_begin + int32_t(b0);
+      w.kv_count = int32_t(b1 - b0);
+      w.split_group = gid;
+      w.split_part = int32_t(p);
+      w.split_parts = int32_t(parts);
+      out.push_back(w);
+    }
+  }
+  std::stable_sort(out.begin(), out.end(),
+                   [](const WorkItem& a, const WorkItem& b) { return a.kv_count > b.kv_count; });
+  S->items.swap(out);
 }
 
 }  // namespace svd
@@ -545,6 +586,8 @@ int svd_plan_get_info(const svd_plan* P, svd_plan_info* info) {
   info->computed_tiles = P->computed_tiles;
   info->active_pairs = P->active_pairs;
   info->dense_pairs = double(P->grid.n) * double(P->grid.n) * double(P->n_heads);
+  info->n_split_groups = P->n_split_groups;
+  info->max_split_parts = P->max_split_parts;
   return SVD_OK;
 }
 
@@ -598,9 +641,11 @@ int svd_plan_schedule(const svd_plan* P, int32_t* items, int32_t* kv) {
   return SVD_OK;
 }
 
-int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** shard) {
+int svd_plan_shard_sm(const svd_plan* P, int32_t world, int32_t rank, int32_t n_sms,
+                      int32_t max_item_tiles, svd_plan** shard) {
   if (!P || !shard) return fail(SVD_ERR_CONFIG, "NULL argument");
   if (world < 1 || rank < 0 || rank >= world) return fail(SVD_ERR_CONFIG, "bad world/rank");
+  if (n_sms < 1) return fail(SVD_ERR_CONFIG, "n_sms must be >= 1");
   auto* S = new svd_plan();
   S->layout = P->layout;
   S->grid = P->grid;
@@ -615,14 +660,23 @@ int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** sh
   S->fine_bit_off = P->fine_bit_off;
   S->active_pairs = P->active_pairs;
   S->sharded = true;
-  // LPT over ranks on the tile cost (items are already heaviest-first)
+  // LPT over ranks on the tile cost (items are already heaviest-first); an
+  // item stays whole across ranks — its split parts (below) share a rank.
+  // Cost in 128-key tile steps + a fixed per-CTA overhead (TMEM / barrier
+  // setup, Q load, pipeline fill, epilogue): short sparse items are not free.
+  auto item_cost = [](const WorkItem& it) {
+    return it.kv_count > 0 ? double(it.kv_count) + kItemOverhead : 0.5 * kItemOverhead;
+  };
   std::vector<double> load(world, 0.0);
-  for (const auto& it : P->items) {
-    const double cost = it.kv_count > 0 ? double(it.kv_count) : 0.05;
-    int32_t best = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
-    load[best] += cost;
-    if (best != rank) continue;
-    WorkItem w = it;
+  std::vector<int32_t> owner(P->items.size());
+  for (size_t i = 0; i < P->items.size(); ++i) {
+    const int32_t best = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
+    load[best] += item_cost(P->items[i]);
+    owner[i] = best;
+  }
+  for (size_t i = 0; i < P->items.size(); ++i) {
+    if (owner[i] != rank) continue;
+    WorkItem w = P->items[i];
     w.out_base = int32_t(S->n_rows);
     for (int k = 0; k < kSlotsPerItem; ++k) {
       if (w.qseg[k] < 0) continue;
@@ -635,10 +689,61 @@ int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** sh
     }
     S->items.push_back(w);
   }
+  // Split-KV cap, one for all ranks: each rank's items are packed onto n_sms
+  // SMs by the hardware's heaviest-first dispatch; when a rank holds only a
+  // few long items per SM (8 GPUs: ~2.6 FULL-row items per SM) that packing
+  // is lumpy (~87% efficiency).  Try caps of 1/4 .. 1/16 of the mean per-SM
+  // load, simulate every rank's dispatch (greedy onto the least-loaded SM,
+  // +2 steps per split part for the merge) and keep the cap with the
+  // smallest slowest-rank makespan.
+  int64_t cap = max_item_tiles;
+  if (cap == 0) {
+    auto makespan = [&](int64_t c) {
+      double worst = 0.0;
+      for (int32_t r = 0; r < world; ++r) {
+        std::vector<double> costs;
+        for (size_t i = 0; i < P->items.size(); ++i) {
+          if (owner[i] != r) continue;
+          const WorkItem& it = P->items[i];
+          const int64_t parts = (c > 0 && it.kv_count > c)
+                                    ? std::min<int64_t>(kMaxSplitParts, (int64_t(it.kv_count) + c - 1) / c)
+                                    : 1;
+          for (int64_t p = 0; p < parts; ++p)
+            costs.push_back(double(it.kv_count) / double(parts) + kItemOverhead + (parts > 1 ? 2.0 : 0.0));
+        }
+        std::sort(costs.begin(), costs.end(), std::greater<double>());
+        std::priority_queue<double, std::vector<double>, std::greater<double>> sm;
+        for (int i = 0; i < n_sms; ++i) sm.push(0.0);
+        for (double c2 : costs) {
+          const double t = sm.top() + c2;
+          sm.pop();
+          sm.push(t);
+          worst = std::max(worst, t);
+        }
+      }
+      return worst;
+    };
+    const double per_sm = *std::max_element(load.begin(), load.end()) / double(n_sms);
+    double best = makespan(-1);
+    cap = -1;
+    for (int div : {4, 6, 8, 12, 16}) {
+      const int64_t c = std::max<int64_t>(32, int64_t(per_sm / div));
+      const double m = makespan(c);
+      if (m < best * 0.995) {
+        best = m;
+        cap = c;
+      }
+    }
+  }
+  split_items(S, cap);
   S->computed_tiles = 0;
   for (const auto& it : S->items) S->computed_tiles += 2 * int64_t(it.kv_count);
   *shard = S;
   return SVD_OK;
+}
+
+int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** shard) {
+  return svd_plan_shard_sm(P, world, rank, 148, 0, shard);
 }
 
 int svd_plan_shard_rows(const svd_plan* S, int64_t* n_rows, int32_t* row_head, int32_t* row_token) {

@@ -35,7 +35,11 @@ struct WorkItem {
   int32_t kv_count;
   int32_t qseg[kSlotsPerItem];  // -1 = empty slot (empty slots form a suffix)
   int32_t out_base;             // packed output row of slot 0 (shards), else -1
-  int32_t pad[3];
+  // split-KV: items whose KV list was cut into parts (to balance SMs in a
+  // shard) carry split group id / part index / part count; -1 / 0 / 1 else
+  int32_t split_group;
+  int32_t split_part;
+  int32_t split_parts;
 };
 static_assert(sizeof(WorkItem) == 48, "WorkItem layout");
 
@@ -77,6 +81,8 @@ struct DeviceTables {
   void* kv = nullptr;
   void* bits = nullptr;
   void* bit_off = nullptr;
+  void* split_scratch = nullptr;  // fp32 partial O [group][part][256][128] + (m, l) [..][256][2]
+  void* split_tickets = nullptr;  // int32 per split group (parts finished), self-resetting
   int64_t n_items = 0;
 };
 
@@ -106,6 +112,7 @@ struct svd_plan {
   // shard view
   bool sharded = false;
   int32_t cluster = 0;  // query segments per work item (kDefaultCluster)
+  int32_t n_split_groups = 0, max_split_parts = 1;
   int64_t n_rows = 0;
   std::vector<int32_t> row_head, row_token;
   // device copies, per CUDA device ordinal

@@ -18,11 +18,11 @@ from . import _native as nat
 from .attention import LayerPlan
 
 
-def gathered_row_maps(plan: LayerPlan, world: int):
+def gathered_row_maps(plan: LayerPlan, world: int, max_item_tiles: int = 0):
     """(shards, row_head, row_token, max_rows) for the all-gathered buffer:
     rank r's packed rows occupy [r*max_rows, (r+1)*max_rows); padding rows and
     rows past the sequence end carry head -1 (skipped by the unpack)."""
-    shards = [plan.shard(world, r) for r in range(world)]
+    shards = [plan.shard(world, r, max_item_tiles=max_item_tiles) for r in range(world)]
     rows = [s.shard_rows() for s in shards]
     max_rows = max(1, max(len(h) for h, _ in rows))
     heads = np.full(world * max_rows, -1, dtype=np.int32)

@@ -200,11 +200,13 @@ def test_deterministic():
     np.testing.assert_array_equal(a, b)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_shard_packed_rows_and_unpack_on_gpu(world):
+@pytest.mark.parametrize("world,split", [(2, False), (3, False), (2, True), (3, True)])
+def test_shard_packed_rows_and_unpack_on_gpu(world, split):
     """The multi-GPU data path on one device: every shard plan writes its
     packed rows, the gathered buffer is unpacked by svd_unpack_rows, and the
-    result equals the single-launch layer output bit for bit."""
+    result equals the single-launch layer output — bit for bit without
+    split-KV; with the planner's split-KV parts (merged in the kernel, a
+    different fp32 summation order) within one bf16 ulp."""
     import torch
 
     from paper_2506_03065_b200 import _native as nat
@@ -217,7 +219,8 @@ def test_shard_packed_rows_and_unpack_on_gpu(world):
     plan = S.LayerPlan.from_specs(specs, S.TokenLayout(*lay))
     ref = torch.empty_like(q)
     plan.forward(q, k, v, ref, head_dim=128)
-    shards, heads, toks, max_rows = gathered_row_maps(plan, world)
+    shards, heads, toks, max_rows = gathered_row_maps(plan, world, max_item_tiles=8 if split else -1)
+    assert (sum(sh.info.n_split_groups for sh in shards) > 0) == split
     gathered = torch.zeros(world * max_rows, 128, dtype=torch.bfloat16, device="cuda")
     for r, sh in enumerate(shards):
         sh.forward(q, k, v, gathered[r * max_rows:(r + 1) * max_rows], head_dim=128)
@@ -228,4 +231,7 @@ def test_shard_packed_rows_and_unpack_on_gpu(world):
         nat.c_void_p(gathered.data_ptr()), int(gathered.stride(0)), nat.c_void_p(out.data_ptr()),
         nat.i64x4(out.stride()), 128, nat.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
-    assert torch.equal(out, ref)
+    if split:
+        torch.testing.assert_close(out.float(), ref.float(), atol=1.6e-2, rtol=8e-3)
+    else:
+        assert torch.equal(out, ref)
