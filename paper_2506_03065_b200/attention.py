@@ -60,7 +60,7 @@ class LayerPlan:
         nat.check(nat.lib().svd_plan_create(nat.make_layout(layout), specs, n, nat.ctypes.byref(out)))
         plan = cls(out.value, layout, n)
         asg = list(assignment)
-        plan._sub = lambda h0, h1: cls.from_specs(asg[h0:h1], layout)
+        plan._sub = lambda heads: cls.from_specs([asg[h] for h in heads], layout)
         return plan
 
     @classmethod
@@ -82,18 +82,23 @@ class LayerPlan:
             nat.ctypes.byref(out)))
         plan = cls(out.value, layout, int(hg.size))
         gm = list(group_masks)
-        plan._sub = lambda h0, h1: cls.from_masks(layout, gm, hg[h0:h1])
+        plan._sub = lambda heads: cls.from_masks(layout, gm, hg[list(heads)])
         return plan
 
     def head_subplan(self, h0: int, h1: int) -> "LayerPlan":
         """The plan restricted to heads [h0, h1) (cached): lets host-resident
         layers be pipelined head-chunk by head-chunk."""
+        return self.heads_subplan(tuple(range(h0, h1)))
+
+    def heads_subplan(self, heads: tuple) -> "LayerPlan":
+        """The plan restricted to the listed heads, in that order (cached)."""
         cache = self.__dict__.setdefault("_subplans", {})
-        if (h0, h1) not in cache:
+        heads = tuple(int(h) for h in heads)
+        if heads not in cache:
             if self._sub is None:
                 raise ConfigError("this plan cannot be split by heads")
-            cache[(h0, h1)] = self._sub(h0, h1)
-        return cache[(h0, h1)]
+            cache[heads] = self._sub(heads)
+        return cache[heads]
 
     # -- queries
     @property
@@ -285,7 +290,116 @@ def _to_device(xs):
     return out, was_numpy, dev
 
 
-HOST_CHUNKS = int(__import__("os").environ.get("SVD_HOST_CHUNKS", "6"))  # head chunks, host pipeline
+# Host-buffer pipeline: head-range chunks flow through copy-in -> kernel ->
+# copy-out.  SVD_HOST_CHUNKS=k forces k equal chunks; by default the
+# boundaries come from a flow-shop model of the three stages (below).
+HOST_CHUNKS = int(__import__("os").environ.get("SVD_HOST_CHUNKS", "0"))
+PCIE_BYTES_PER_S = float(__import__("os").environ.get("SVD_PCIE_GBPS", "50")) * 1e9
+# Per-SM kernel time per KV step of a work item (two 128-row tiles x 128
+# keys), measured on B200 at power-capped clocks: HunyuanVideo 40.5 ms x 148
+# SMs / 2.89 M steps (d=128), CogVideoX 35.7 ms x 148 / 3.48 M (d=64); plus a
+# fixed per-CTA cost (TMEM / barrier setup, Q load, epilogue).
+STEP_SECONDS = {64: 1.52e-6, 128: 2.07e-6}
+ITEM_SECONDS = 5e-6
+LAUNCH_SECONDS = 15e-6
+
+
+def _flow_shop(bounds, h2d, kernel, d2h) -> float:
+    """Makespan of chunks [bounds[i], bounds[i+1]) of a head order through
+    three in-order stages (H2D stream, compute stream, D2H stream; PCIe is
+    full duplex).  kernel(a, b): modelled launch time of order[a:b]."""
+    t1 = t2 = t3 = 0.0
+    for c in range(len(bounds) - 1):
+        a, b = bounds[c], bounds[c + 1]
+        t1 += h2d * (b - a)
+        t2 = max(t2, t1) + kernel(a, b)
+        t3 = max(t3, t2) + d2h * (b - a)
+    return t3
+
+
+def _launch_model(plan: "LayerPlan", B: int, d: int):
+    """Per head: (SM-seconds of work, longest item in seconds).  A launch of
+    a head set takes max(total work / SMs, longest item) + launch latency:
+    every head of a text/frame layout has full-length forced rows, so a
+    launch of a few sparse heads is bound by its longest item, not its work."""
+    step = STEP_SECONDS[_tensor_dim(d)]
+    work, longest = [], []
+    for h in range(plan.n_heads):
+        items, _ = plan.heads_subplan((h,)).schedule()
+        kv = items[:, 3].astype(np.float64) if len(items) else np.zeros(1)
+        work.append(B * float(np.sum(kv * step + ITEM_SECONDS)))
+        longest.append(float(kv.max()) * step + ITEM_SECONDS)
+    return work, longest
+
+
+def _host_schedule(plan: LayerPlan, B: int, N: int, d: int):
+    """(head order, chunk boundaries) for the host pipeline.
+
+    Stage times per head: H2D 3*B*N*d*2 bytes, the kernel by the head's
+    issued tiles (a FULL head costs ~30x a sparse one), D2H B*N*d*2 bytes.
+    Heads are ordered by Johnson's rule for the copy-in -> kernel flow shop
+    (kernel-heavy heads first, so the kernel starts early and the copies of
+    the light heads hide under it; then the rest by falling kernel time), and
+    the chunk boundaries by local search from equal chunks (a small first
+    chunk starts the kernel early, a small last one shortens the drain)."""
+    H = plan.n_heads
+    cache = plan.__dict__.setdefault("_host_sched", {})
+    key = (B, N, d, HOST_CHUNKS)
+    if key in cache:
+        return cache[key]
+    h2d = 3 * B * N * d * 2 / PCIE_BYTES_PER_S
+    d2h = B * N * d * 2 / PCIE_BYTES_PER_S
+    if HOST_CHUNKS > 0:
+        order = list(range(H))
+        k = max(1, min(HOST_CHUNKS, H))
+        bounds = [round(i * H / k) for i in range(k + 1)]
+    else:
+        work, longest = _launch_model(plan, B, d)
+        sms = _device_sm_count()
+        solo = [max(w / sms, t) for w, t in zip(work, longest)]
+        heavy = sorted((h for h in range(H) if solo[h] >= h2d), key=lambda h: (-solo[h], h))
+        light = sorted((h for h in range(H) if solo[h] < h2d), key=lambda h: (-solo[h], h))
+        best_all = None
+        for cand_order in (heavy + light, list(range(H))):  # Johnson's order, the given order
+            wpre = [0.0]
+            for h in cand_order:
+                wpre.append(wpre[-1] + work[h])
+
+            def kernel(a, b, o=cand_order, wp=wpre):
+                return max((wp[b] - wp[a]) / sms, max(longest[h] for h in o[a:b])) + LAUNCH_SECONDS
+
+            def cost(bd, kernel=kernel):
+                return _flow_shop(bd, h2d, kernel, d2h)
+
+            best, best_cost = None, float("inf")
+            for k in range(1, min(H, 12) + 1):
+                bd = [round(i * H / k) for i in range(k + 1)]
+                c = cost(bd)
+                if c < best_cost:
+                    best, best_cost = bd, c
+            improved = True
+            while improved:  # boundary moves, merges and splits
+                improved = False
+                cands = []
+                for i in range(1, len(best) - 1):
+                    for delta in (-2, -1, 1, 2):
+                        nb = list(best)
+                        nb[i] += delta
+                        if nb[i - 1] < nb[i] < nb[i + 1]:
+                            cands.append(nb)
+                    cands.append(best[:i] + best[i + 1:])
+                for i in range(len(best) - 1):
+                    if best[i + 1] - best[i] > 1:
+                        cands.append(best[:i + 1] + [(best[i] + best[i + 1]) // 2] + best[i + 1:])
+                for nb in cands:
+                    c = cost(nb)
+                    if c < best_cost * 0.999:
+                        best, best_cost, improved = nb, c, True
+            if best_all is None or best_cost < best_all[0]:
+                best_all = (best_cost, cand_order, best)
+        _, order, bounds = best_all
+    cache[key] = (order, bounds)
+    return order, bounds
 
 
 class _Staging:
@@ -337,13 +451,14 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
     B, H, N, d = q.shape
     dev = torch.device("cuda", torch.cuda.current_device())
     D = _tensor_dim(d)
-    chunks = max(1, min(HOST_CHUNKS, H))
-    bounds = [round(i * H / chunks) for i in range(chunks + 1)]
+    order, bounds = _host_schedule(plan, B, N, d)
+    chunks = len(bounds) - 1
     if out is None:
         out_host = torch.empty((B, H, N, d), dtype=torch.bfloat16, pin_memory=True)
     else:
         _check_out(out, (B, H, N, d), "cpu")
         out_host = out
+    # staging slot s holds head order[s]; chunks are contiguous slot ranges
     st = _host_staging(plan, dev, B, N, d, D)
     with st.lock:
         compute = torch.cuda.current_stream(dev)
@@ -351,31 +466,33 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
         loaded = []
         with torch.cuda.stream(s_in):
             for c in range(chunks):
-                h0, h1 = bounds[c], bounds[c + 1]
-                for x, buf in zip((q, k, v), st.qkv):
-                    xc = x[:, h0:h1]
-                    if xc.dtype != torch.bfloat16:
-                        xc = xc.to(torch.bfloat16)
-                    if not xc.is_pinned():
-                        xc = xc.contiguous().pin_memory()
-                    buf[:, h0:h1, :, :d].copy_(xc, non_blocking=True)
+                for slot in range(bounds[c], bounds[c + 1]):
+                    h = order[slot]
+                    for x, buf in zip((q, k, v), st.qkv):
+                        xc = x[:, h]
+                        if xc.dtype != torch.bfloat16:
+                            xc = xc.to(torch.bfloat16)
+                        if not xc.is_pinned():
+                            xc = xc.contiguous().pin_memory()
+                        buf[:, slot, :, :d].copy_(xc, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(s_in)
                 loaded.append(ev)
         computed = []
         for c in range(chunks):
-            h0, h1 = bounds[c], bounds[c + 1]
+            s0, s1 = bounds[c], bounds[c + 1]
             compute.wait_event(loaded[c])
-            qc, kc, vc = (buf[:, h0:h1] for buf in st.qkv)
-            plan.head_subplan(h0, h1).forward(qc, kc, vc, st.o[:, h0:h1], head_dim=d, stream=compute)
+            qc, kc, vc = (buf[:, s0:s1] for buf in st.qkv)
+            plan.heads_subplan(tuple(order[s0:s1])).forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d,
+                                                             stream=compute)
             ev = torch.cuda.Event()
             ev.record(compute)
             computed.append(ev)
         with torch.cuda.stream(s_out):
             for c in range(chunks):
-                h0, h1 = bounds[c], bounds[c + 1]
                 s_out.wait_event(computed[c])
-                out_host[:, h0:h1].copy_(st.o[:, h0:h1, :, :d], non_blocking=True)
+                for slot in range(bounds[c], bounds[c + 1]):
+                    out_host[:, order[slot]].copy_(st.o[:, slot, :, :d], non_blocking=True)
         s_out.synchronize()  # a host result must be readable on return
     return out_host
 

@@ -113,3 +113,32 @@ def test_layer_plan_flops_match_reference_convention():
     g = S.block_grid(layout)
     want = sum(S.attention_flops(4096, 64, 1, S.sparsity(s, g)) for s in asg if s.mode is not S.Mode.SKIP)
     assert plan.active_flops(64) == pytest.approx(want, rel=1e-12)
+
+
+def test_host_pipeline_schedule_is_a_partition_and_beats_equal_chunks():
+    """The host-buffer pipeline's head order is a permutation, its chunks
+    partition it, and the modelled makespan is no worse than 6 equal chunks
+    (attention._host_schedule; runs on CPU — plans need no GPU)."""
+    from paper_2506_03065_b200 import attention as A
+
+    layout = S.TokenLayout(256, 33, 3600, 64)
+    asg = ([S.multi_diagonal_spec(), S.diagonal_spec(1)] * 3 + [S.full_spec()] * 2 + [S.skip_spec()]
+           + [S.vertical_stripe_spec(stripes=(5, 900))] + [S.full_spec()] * 2)
+    plan = S.plan_for_assignment(asg, layout)
+    H, N, d = len(asg), layout.total_tokens, 128
+    order, bounds = A._host_schedule(plan, 1, N, d)
+    assert sorted(order) == list(range(H))
+    assert bounds[0] == 0 and bounds[-1] == H and all(a < b for a, b in zip(bounds, bounds[1:]))
+    work, longest = A._launch_model(plan, 1, d)
+    sms = A._device_sm_count()
+    h2d, d2h = 3 * N * d * 2 / A.PCIE_BYTES_PER_S, N * d * 2 / A.PCIE_BYTES_PER_S
+
+    def makespan(o, bd):
+        def kernel(a, b):
+            return max(sum(work[h] for h in o[a:b]) / sms, max(longest[h] for h in o[a:b])) + A.LAUNCH_SECONDS
+        return A._flow_shop(bd, h2d, kernel, d2h)
+
+    equal = [round(i * H / 6) for i in range(7)]
+    assert makespan(order, bounds) <= makespan(list(range(H)), equal) + 1e-9
+    # sub-plans of a head subset keep each head's schedule: same work as the full plan
+    assert sum(plan.heads_subplan((h,)).info.computed_tiles for h in range(H)) == plan.info.computed_tiles
