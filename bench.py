@@ -424,7 +424,8 @@ def run_ours(args):
             "wall_ms_steps": e2e_walls,
             "h2d_bytes_per_step": 3 * H * n * d * 2,
             "d2h_bytes_per_step": H * n * d * 2,
-            "path": "fused_layer_attention(pinned host bf16 Q/K/V): head-chunk pipelined H2D / kernel / D2H",
+            "path": ("fused_layer_attention(pinned host bf16 Q/K/V, out=pinned O): heads reordered and "
+                     "chunked by a flow-shop model, H2D / kernel / D2H streams overlapped"),
         },
         "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),
         "clocks": clock,

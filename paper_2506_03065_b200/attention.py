@@ -359,44 +359,67 @@ def _host_schedule(plan: LayerPlan, B: int, N: int, d: int):
         solo = [max(w / sms, t) for w, t in zip(work, longest)]
         heavy = sorted((h for h in range(H) if solo[h] >= h2d), key=lambda h: (-solo[h], h))
         light = sorted((h for h in range(H) if solo[h] < h2d), key=lambda h: (-solo[h], h))
-        best_all = None
-        for cand_order in (heavy + light, list(range(H))):  # Johnson's order, the given order
-            wpre = [0.0]
-            for h in cand_order:
-                wpre.append(wpre[-1] + work[h])
+        hpre = {}
 
-            def kernel(a, b, o=cand_order, wp=wpre):
+        def cost(o, bd):
+            wp = [0.0]
+            for h in o:
+                wp.append(wp[-1] + work[h])
+
+            def kernel(a, b):
                 return max((wp[b] - wp[a]) / sms, max(longest[h] for h in o[a:b])) + LAUNCH_SECONDS
 
-            def cost(bd, kernel=kernel):
-                return _flow_shop(bd, h2d, kernel, d2h)
+            return _flow_shop(bd, h2d, kernel, d2h)
 
-            best, best_cost = None, float("inf")
-            for k in range(1, min(H, 12) + 1):
-                bd = [round(i * H / k) for i in range(k + 1)]
-                c = cost(bd)
-                if c < best_cost:
-                    best, best_cost = bd, c
+        def improve_bounds(o, bd, c0):
             improved = True
             while improved:  # boundary moves, merges and splits
                 improved = False
                 cands = []
-                for i in range(1, len(best) - 1):
+                for i in range(1, len(bd) - 1):
                     for delta in (-2, -1, 1, 2):
-                        nb = list(best)
+                        nb = list(bd)
                         nb[i] += delta
                         if nb[i - 1] < nb[i] < nb[i + 1]:
                             cands.append(nb)
-                    cands.append(best[:i] + best[i + 1:])
-                for i in range(len(best) - 1):
-                    if best[i + 1] - best[i] > 1:
-                        cands.append(best[:i + 1] + [(best[i] + best[i + 1]) // 2] + best[i + 1:])
+                    cands.append(bd[:i] + bd[i + 1:])
+                for i in range(len(bd) - 1):
+                    if bd[i + 1] - bd[i] > 1:
+                        cands.append(bd[:i + 1] + [(bd[i] + bd[i + 1]) // 2] + bd[i + 1:])
                 for nb in cands:
-                    c = cost(nb)
-                    if c < best_cost * 0.999:
-                        best, best_cost, improved = nb, c, True
-            if best_all is None or best_cost < best_all[0]:
-                best_all = (best_cost, cand_order, best)
+                    c = cost(o, nb)
+                    if c < c0 * 0.999:
+                        bd, c0, improved = nb, c, True
+            return bd, c0
+
+        best_all = None
+        for cand_order in (heavy + light, list(range(H))):  # Johnson's order, the given order
+            bd, c0 = None, float("inf")
+            for k in range(1, min(H, 12) + 1):
+                nb = [round(i * H / k) for i in range(k + 1)]
+                c = cost(cand_order, nb)
+                if c < c0:
+                    bd, c0 = nb, c
+            bd, c0 = improve_bounds(cand_order, bd, c0)
+            if best_all is None or c0 < best_all[0]:
+                best_all = (c0, list(cand_order), bd)
+        # then alternate: head moves between chunks (first improvement), bounds
+        c0, o, bd = best_all
+        for _ in range(8):
+            moved = False
+            for i in range(H):
+                for j in range(H):
+                    if i == j:
+                        continue
+                    no = list(o)
+                    no.insert(j, no.pop(i))
+                    c = cost(no, bd)
+                    if c < c0 * 0.999:
+                        o, c0, moved = no, c, True
+            bd, c0 = improve_bounds(o, bd, c0)
+            if not moved:
+                break
+        best_all = (c0, o, bd)
         _, order, bounds = best_all
     cache[key] = (order, bounds)
     return order, bounds
