@@ -46,7 +46,8 @@ class PeerShardedLayer:
     then complete).
     """
 
-    def __init__(self, plan: LayerPlan, world: int, rank: int, head_dim: int, device, shape):
+    def __init__(self, plan: LayerPlan, world: int, rank: int, head_dim: int, device, shape,
+                 max_item_tiles: int | None = None):
         import torch
         import torch.distributed as dist
 
@@ -55,7 +56,12 @@ class PeerShardedLayer:
         self.rank = rank
         self.head_dim = head_dim
         self.device = device
-        self.shard = plan.shard(world, rank) if world > 1 else plan
+        # a shard view (split-KV balanced) for N > 1, the plain plan for one rank
+        # unless a split cap is forced (tests)
+        if world > 1 or max_item_tiles is not None:
+            self.shard = plan.shard(world, rank, max_item_tiles=max_item_tiles or 0)
+        else:
+            self.shard = plan
         self.out = torch.empty(shape, dtype=torch.bfloat16, device=device)
         off = nat.c_int64(0)
         buf = (nat.c_uint8 * 64)()
