@@ -12,9 +12,9 @@ import paper_2506_03065_b200 as S
 
 ROOT = Path(__file__).resolve().parent.parent
 
-# kernel-only B200 measurements of the default build (profiles/r1/ab2.log,
+# kernel-only B200 measurements of the current build (profiles/r1/costmodel_sweep.log run,
 # scripts/time_layers.py, same session as the sweep's kernel version)
-MEASURED_MS = {"hunyuan": 43.3, "cogvideo": 35.9, "wan": 47.1}
+MEASURED_MS = {"hunyuan": 41.1, "cogvideo": 36.3, "wan": 44.8}
 
 
 def test_shipped_fit_exists_and_is_sane():
