@@ -30,7 +30,7 @@ nat.check(lib.svd_debug_trace(None, 0, 1))
 plan.forward(q, k, v, out, head_dim=d)
 nat.check(lib.svd_debug_trace(buf.ctypes.data, buf.nbytes, 0))
 names = {0: "top", 1: "S-ready", 3: "S-loaded", 4: "max-done", 6: "P0", 2: "P1",
-         30: "wait-P0", 40: "got-P0", 50: "got-P1", 10: "PV-issued", 60: "K-ready", 61: "S-issued",
+         30: "wait-P", 40: "got-P", 50: "got-P1", 10: "PV-issued", 60: "K-ready", 61: "S-issued",
          20: "S-commit", 21: "S-commit", 70: "K-slot-free"}
 ev = []
 cta = 0
