@@ -147,11 +147,63 @@ def ncu_traffic(cfg_key: str):
 
 
 # ----------------------------------------------------------------- CPU baseline (oracle port)
+_CPU = {}  # per-worker state of the CPU baseline (built once by _cpu_init)
+
+
+def _cpu_init(layout, d, mode_specs):
+    """Spawned-worker initializer: the oracle, the grid, seeded Q/K/V (one
+    head at full N) and the per-mode masks — rebuilt in every worker, so the
+    pool never inherits the parent's CUDA / BLAS thread state."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import svdit_oracle as O
+
+    og = O.block_grid(*layout)
+    rng = np.random.default_rng(0)
+    _CPU.update(O=O, grid=og,
+                q=rng.standard_normal((1, 1, og.n, d), dtype=np.float32),
+                k=rng.standard_normal((1, 1, og.n, d), dtype=np.float32),
+                v=rng.standard_normal((1, 1, og.n, d), dtype=np.float32),
+                active={m: O.build_mask(sp, og) for m, sp in mode_specs.items()})
+
+
+def _cpu_worker(args):
+    """One process of the CPU baseline: the oracle's streaming attention on
+    its share of the query blocks, one BLAS thread, until the time slice ends."""
+    m, qbs, slice_s = args
+    O = _CPU["O"]
+    try:
+        from threadpoolctl import threadpool_limits
+
+        limiter = threadpool_limits(1)
+    except ImportError:  # single-threaded BLAS anyway once forked per core
+        limiter = None
+    og, q, k, v = _CPU["grid"], _CPU["q"], _CPU["k"], _CPU["v"]
+    active = _CPU["active"][m]
+    d = q.shape[-1]
+    t0 = time.perf_counter()
+    done = 0.0
+    nq = 0
+    for qb in qbs:
+        O.sparse_attention_rows(q, k, v, active, og.bounds, [int(qb)])
+        rows = og.bounds[qb + 1] - og.bounds[qb]
+        done += 4.0 * d * rows * float(np.diff(og.bounds)[active[qb]].sum())
+        nq += 1
+        if time.perf_counter() - t0 > slice_s:
+            break
+    if limiter is not None:
+        limiter.restore_original_limits()
+    return done, time.perf_counter() - t0, nq
+
+
 def cpu_baseline(cfg, S, budget_s: float = 15.0) -> dict:
     """Time the reference algorithm (fp64 streaming online softmax, the oracle
-    port of attention.py:57-98) on this host over a bounded sample of query
-    blocks of one head per distinct mode at full N, and extrapolate to the
-    whole layer by active FLOPs per mode."""
+    port of attention.py:57-98) on this host's cores over a bounded sample of
+    query blocks of one head per distinct mode at full N, and extrapolate to
+    the whole layer by active FLOPs per mode.  Query blocks are independent
+    (attention.py:81-97), so one forked worker per core runs the unchanged
+    per-block algorithm with one BLAS thread each."""
+    import multiprocessing as mp
+
     sys.path.insert(0, str(ROOT / "oracle"))
     import svdit_oracle as O
 
@@ -159,54 +211,55 @@ def cpu_baseline(cfg, S, budget_s: float = 15.0) -> dict:
     og = O.block_grid(text, frames, tpf, bs)
     n, d = og.n, cfg["d"]
     specs = assignment_for(cfg, S)
-    rng = np.random.default_rng(0)
-    q = rng.standard_normal((1, 1, n, d), dtype=np.float32)
-    k = rng.standard_normal((1, 1, n, d), dtype=np.float32)
-    v = rng.standard_normal((1, 1, n, d), dtype=np.float32)
+    rng = np.random.default_rng(1)
     per_mode = {}
     for spec in specs:
         per_mode.setdefault(int(spec.mode), spec)
     modes = [m for m in per_mode if m != 1]
+    workers = max(1, os.cpu_count() or 1)
     slice_s = budget_s / max(1, len(modes))
     total_flops_layer = 0.0
     total_time_layer = 0.0
     sampled = []
-    for m in modes:
-        spec = per_mode[m]
-        active = O.build_mask(spec, og)
-        heads_m = sum(1 for s in specs if int(s.mode) == m)
-        # layer FLOPs of this mode (all its heads; stripe heads differ only in columns)
-        flops_mode = sum(4.0 * d * O.active_pairs(O.build_mask(s, og), og.bounds)
-                         for s in specs if int(s.mode) == m)
-        order = rng.permutation(og.n_blocks)
-        t0 = time.perf_counter()
-        done_flops = 0.0
-        nq = 0
-        for qb in order:
-            O.sparse_attention_rows(q, k, v, active, og.bounds, [int(qb)])
-            rows = og.bounds[qb + 1] - og.bounds[qb]
-            cols = float(np.diff(og.bounds)[active[qb]].sum())
-            done_flops += 4.0 * d * rows * cols
-            nq += 1
-            if time.perf_counter() - t0 > slice_s:
-                break
-        dt = time.perf_counter() - t0
-        rate = done_flops / dt
-        total_flops_layer += flops_mode
-        total_time_layer += flops_mode / rate
-        sampled.append(f"{S.Mode(m).label}:{nq}qb/{heads_m}h "
-                       f"{rate / 1e9:.1f}GF/s")
+    ctx = mp.get_context("spawn")
+    env_blas = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_blas:  # spawned workers start with single-threaded BLAS
+        os.environ[k] = "1"
+    try:
+        pool = ctx.Pool(workers, initializer=_cpu_init,
+                        initargs=(cfg["layout"], d, {m: per_mode[m] for m in modes}))
+    finally:
+        for k, val in env_blas.items():
+            if val is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = val
+    with pool:
+        for m in modes:
+            heads_m = sum(1 for s in specs if int(s.mode) == m)
+            flops_mode = sum(4.0 * d * O.active_pairs(O.build_mask(s, og), og.bounds)
+                             for s in specs if int(s.mode) == m)
+            order = rng.permutation(og.n_blocks)
+            shares = [order[w::workers] for w in range(workers)]
+            res = pool.map(_cpu_worker, [(m, sh, slice_s) for sh in shares])
+            done = sum(r[0] for r in res)
+            wall = max(r[1] for r in res)
+            nq = sum(r[2] for r in res)
+            rate = done / wall
+            total_flops_layer += flops_mode
+            total_time_layer += flops_mode / rate
+            sampled.append(f"{S.Mode(m).label}:{nq}qb/{heads_m}h {rate / 1e9:.1f}GF/s")
     dense = 4.0 * n * n * d * cfg["heads"]
     return {
         "value": dense / total_time_layer / 1e12,
         "unit": "TFLOP/s (dense-equivalent)",
         "ms_per_layer": total_time_layer * 1e3,
         "active_gflops_per_s": total_flops_layer / total_time_layer / 1e9,
-        "cores": os.cpu_count(),
+        "cores": workers,
         "kind": "port",
         "sample": (f"fp64 NumPy oracle (attention.py:57-98 restated), 1 head per mode at full N={n}, "
-                   f"random query blocks for ~{slice_s:.0f}s each [{'; '.join(sampled)}], "
-                   f"extrapolated by active FLOPs; BLAS threads = all {os.cpu_count()} host cores"),
+                   f"random query blocks for ~{slice_s:.0f}s each on {workers} worker processes x 1 BLAS "
+                   f"thread [{'; '.join(sampled)}], extrapolated by active FLOPs"),
     }
 
 
