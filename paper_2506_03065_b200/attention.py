@@ -602,7 +602,7 @@ def group_heads(assignment, grid: BlockGrid) -> list[HeadGroup]:
         heads, skip = plan.group_heads(g)
         spec = assignment[heads[0]]
         mask = None
-        if spec.mode not in (Mode.FULL, Mode.SKIP):
+        if int(spec.mode) not in (Mode.FULL, Mode.SKIP):
             mask = BlockMask(grid=grid, active=plan.group_mask(g))
         groups.append(HeadGroup(spec=spec, heads=heads, mask=mask, plan=plan))
     _GROUP_CACHE[key] = groups
@@ -626,9 +626,9 @@ def _plan_for_groups(groups, H: int, N: int) -> LayerPlan:
     for gi, g in enumerate(groups):
         if g.mask is not None:
             layout = g.mask.grid.layout
-        if g.spec.mode is Mode.SKIP:
+        if int(g.spec.mode) == Mode.SKIP:
             masks.append(None)
-        elif g.spec.mode is Mode.FULL or g.mask is None:
+        elif int(g.spec.mode) == Mode.FULL or g.mask is None:
             masks.append("full")
         else:
             masks.append(g.mask.active)

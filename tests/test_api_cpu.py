@@ -4,6 +4,7 @@ reference's exception classes before any device work (attention.py:27-33,
 model, and the no-CPU-fallback guarantee."""
 
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -142,3 +143,35 @@ def test_host_pipeline_schedule_is_a_partition_and_beats_equal_chunks():
     assert makespan(order, bounds) <= makespan(list(range(H)), equal) + 1e-9
     # sub-plans of a head subset keep each head's schedule: same work as the full plan
     assert sum(plan.heads_subplan((h,)).info.computed_tiles for h in range(H)) == plan.info.computed_tiles
+
+
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference package not mounted (build container only)")
+def test_drop_in_accepts_the_reference_objects():
+    """A maintainer swapping the imports hands OUR functions the REFERENCE's
+    own TokenLayout / BlockGrid / PatternSpec objects (model.py:405-420,
+    search.py:142-143): grids, masks, sparsities and grouping come out equal."""
+    import sys
+
+    sys.path.insert(0, str(REF_SRC))
+    from svdit import attention as RA
+    from svdit import layout as RL
+    from svdit import patterns as RP
+
+    lay = RL.TokenLayout(96, 8, 250, 64)
+    rgrid = RL.block_grid(lay)
+    g = S.block_grid(lay)
+    np.testing.assert_array_equal(g.bounds, rgrid.bounds)
+    np.testing.assert_array_equal(g.forced, rgrid.forced)
+    specs = [RP.full_spec(), RP.diagonal_spec(1), RP.skip_spec(), RP.multi_diagonal_spec(),
+             RP.vertical_stripe_spec(stripes=(2, 20))]
+    for grid in (g, rgrid):
+        ours, ref = S.group_heads(specs, grid), RA.group_heads(specs, rgrid)
+        assert [x.heads for x in ours] == [x.heads for x in ref]
+        for a, b in zip(ours, ref):
+            if b.mask is not None:
+                np.testing.assert_array_equal(np.asarray(a.mask.active), b.mask.active)
+    for sp in specs:
+        assert S.sparsity(sp, g) == RP.sparsity(sp, rgrid)
