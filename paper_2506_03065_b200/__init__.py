@@ -53,6 +53,7 @@ from .search import (
     SPARSE_MODES,
     PatternConfig,
     SearchParams,
+    aggregate_config,
     config_sparsity,
     mode_loss,
     select_mode,

@@ -612,8 +612,9 @@ def group_heads(assignment, grid: BlockGrid) -> list[HeadGroup]:
 
 
 def _plan_for_groups(groups, H: int, N: int) -> LayerPlan:
-    plans = {id(g.plan) for g in groups}
-    first = groups[0].plan
+    # groups may also be the reference's own HeadGroups (no plan attached)
+    plans = {id(getattr(g, "plan", None)) for g in groups}
+    first = getattr(groups[0], "plan", None)
     if len(plans) == 1 and first is not None and first.n_heads == H:
         # the groups came from one group_heads() call: check they are that plan's
         info = first.info

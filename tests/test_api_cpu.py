@@ -175,3 +175,71 @@ def test_drop_in_accepts_the_reference_objects():
                 np.testing.assert_array_equal(np.asarray(a.mask.active), b.mask.active)
     for sp in specs:
         assert S.sparsity(sp, g) == RP.sparsity(sp, rgrid)
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference package not mounted (build container only)")
+def test_reference_head_groups_lower_to_the_same_plan():
+    """fused_layer_attention also takes HeadGroups built by the REFERENCE's
+    group_heads (attention.py:164-183): they lower to a plan with the same
+    grouping, masks and kernel work as our own group_heads gives."""
+    import sys
+
+    sys.path.insert(0, str(REF_SRC))
+    from svdit import attention as RA
+    from svdit import layout as RL
+    from svdit import patterns as RP
+
+    from paper_2506_03065_b200 import attention as A
+
+    lay = RL.TokenLayout(20, 6, 300, 64)
+    specs = [RP.full_spec(), RP.skip_spec(), RP.diagonal_spec(2), RP.vertical_stripe_spec(stripes=(3, 17)),
+             RP.diagonal_spec(2), RP.multi_diagonal_spec()]
+    ref_groups = RA.group_heads(specs, RL.block_grid(lay))
+    plan = A._plan_for_groups(ref_groups, len(specs), lay.total_tokens)
+    ours = S.plan_for_assignment(specs, S.TokenLayout(20, 6, 300, 64))
+    assert plan.info.n_groups == ours.info.n_groups == len(ref_groups)
+    assert plan.info.computed_tiles == ours.info.computed_tiles
+    for g, rg in enumerate(ref_groups):
+        assert plan.group_heads(g)[0] == rg.heads
+        if rg.mask is not None:
+            np.testing.assert_array_equal(plan.group_mask(g), rg.mask.active)
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference package not mounted (build container only)")
+def test_plugin_surface_matches_the_reference():
+    """The search / cost-model plugin surface gives the reference's numbers on
+    the same inputs: attention_flops, layer_linear_flops,
+    attention_latency_share (costmodel.py:26-50), mode_loss, select_mode
+    (search.py:65-103), sparsity_table, config_sparsity, aggregate_config
+    (search.py:233-299) — for a random strategy table with stripe heads."""
+    import sys
+
+    sys.path.insert(0, str(REF_SRC))
+    from svdit import costmodel as RC
+    from svdit import layout as RL
+    from svdit import patterns as RP
+    from svdit import search as RS
+
+    for n, d, h, sp in [(4096, 64, 8, 0.2), (119056, 128, 24, 0.72), (85906, 64, 48, 0.0)]:
+        assert S.attention_flops(n, d, h, sp) == RC.attention_flops(n, d, h, sp)
+        assert S.layer_linear_flops(n, d * h) == RC.layer_linear_flops(n, d * h)
+        assert S.attention_latency_share(n, d, h) == RC.attention_latency_share(n, d, h)
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        losses = rng.choice([0.1, 0.2, 0.2, 0.5], size=4)
+        spars = rng.choice([0.0, 0.5, 0.9, 0.9], size=4)
+        eps = float(rng.choice([0.05, 0.2, 1.0]))
+        assert int(S.select_mode(losses, spars, eps)) == int(RS.select_mode(losses, spars, eps))
+    a, b = rng.standard_normal((2, 3, 50, 8)).astype(np.float32)
+    for pen in ("eq2_density", "alg1_sparsity"):
+        assert S.mode_loss(a, b, 0.3, 0.5, pen) == pytest.approx(RS.mode_loss(a, b, 0.3, 0.5, pen), rel=1e-12)
+    modes = rng.integers(0, 5, size=(4, 3, 5)).astype(np.uint8)
+    stripes = {(l, hh): (1 + l, 7 + hh) for l in range(3) for hh in range(5)}
+    lay_ours, lay_ref = S.TokenLayout(32, 6, 200, 64), RL.TokenLayout(32, 6, 200, 64)
+    ours = S.PatternConfig(modes=modes, stripes=stripes)
+    ref = RS.PatternConfig(modes=modes, stripes=stripes, params=RP.PatternParams())
+    np.testing.assert_array_equal(S.sparsity_table(ours, lay_ours), RS.sparsity_table(ref, lay_ref))
+    assert S.config_sparsity(ours, lay_ours) == RS.config_sparsity(ref, lay_ref)
+    for strat in ("per_step", "majority_over_steps"):
+        np.testing.assert_array_equal(S.aggregate_config(ours, lay_ours, strat).modes,
+                                      RS.aggregate_config(ref, lay_ref, strat).modes)
