@@ -332,11 +332,26 @@ def run_ours(args):
     # all-gather + unpack
     mgpu = os.environ.get("SVD_MULTI_GPU", "p2p") if world > 1 else "single"
     if mgpu == "p2p":
+        import torch.distributed as dist
+
         from paper_2506_03065_b200.sharding import PeerShardedLayer
 
-        layer = PeerShardedLayer(plan, world, rank, d, dev, (1, H, n, d))
-        out = layer.out
-    else:
+        try:
+            layer = PeerShardedLayer(plan, world, rank, d, dev, (1, H, n, d))
+            ok = 1
+        except Exception as exc:  # no peer access between these GPUs: NCCL path
+            print(f"rank {rank}: peer-memory path unavailable ({exc}); using NCCL all-gather",
+                  file=sys.stderr)
+            layer, ok = None, 0
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag[0]) == 1:
+            out = layer.out
+        else:
+            if layer is not None:
+                layer.close()
+            mgpu = "nccl"
+    if mgpu != "p2p":  # one GPU, or packed rows + NCCL all-gather + unpack
         layer = HeadShardedLayer(plan, world, rank, head_dim=d, device=dev)
         out = torch.empty(1, H, n, d, device=dev, dtype=torch.bfloat16)
     stream = torch.cuda.current_stream(dev)
