@@ -178,17 +178,36 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
   }
 }
 
-// Exp2 offload: of every 8 consecutive column pairs, the last kEmuPairs go
-// through the FMA-pipe polynomial instead of MUFU.ex2 (MUFU is 16/clk/SM and
-// would otherwise co-limit with the tensor pipe).
+// Exp2 offload: of every 8 consecutive column pairs, kEmuPairs go through
+// the FMA-pipe polynomial instead of MUFU.ex2 (MUFU is 16/clk/SM, as fast as
+// the tensor pipe needs at d=128).  Default d=128: the first 3 of every 8
+// pairs (their longer dependency chains start first), minimax quadratic —
+// -3.5% layer time (profiles/r1/KERNEL_NOTES.md); d=64: off (measured slower).
 #ifndef SVD_EMU128
-#define SVD_EMU128 0
+#define SVD_EMU128 3
 #endif
 #ifndef SVD_EMU64
 #define SVD_EMU64 0
 #endif
 template <int D>
 constexpr int kEmuPairs = D == 128 ? SVD_EMU128 : SVD_EMU64;
+// which pairs of each 8 are emulated: 0 = the last kEmuPairs, 1 = the first
+// (their long dependency chains start early), 2 = spread evenly, 3 = the first
+// 2*kEmuPairs of each 16
+#ifndef SVD_EMU_FIRST
+#define SVD_EMU_FIRST 1
+#endif
+#ifndef SVD_EMU_DEG2
+#define SVD_EMU_DEG2 1
+#endif
+template <int D>
+__device__ __forceinline__ constexpr bool emulated_pair(int i) {
+  return kEmuPairs<D> == 0 ? false
+         : SVD_EMU_FIRST == 1 ? ((i & 7) < kEmuPairs<D>)
+         : SVD_EMU_FIRST == 2 ? ((i & 7) % (8 / kEmuPairs<D>) == 0)
+         : SVD_EMU_FIRST == 3 ? ((i & 15) < 2 * kEmuPairs<D>)
+                              : ((i & 7) >= 8 - kEmuPairs<D>);
+}
 
 #ifdef SVD_TRACE
 // Debug-only pipeline trace: (clock, step<<8 | event) pairs for the first 8
@@ -460,8 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 16; ++i) {
       const float2 xv = ptx::ffma2(make_float2(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]), sl2x2, nm);
       float2 pv;
-      if ((i & 7) >= 8 - kEmuPairs<D>) {
-        pv = ptx::ex2_poly2(xv);
+      if (emulated_pair<D>(i)) {
+        pv = SVD_EMU_DEG2 ? ptx::ex2_poly2_deg2(xv) : ptx::ex2_poly2(xv);
       } else {
         pv.x = ptx::ex2(xv.x);
         pv.y = ptx::ex2(xv.y);
