@@ -43,6 +43,11 @@ constexpr uint32_t kTmemCols = 512;
 // Row sums over the bf16-rounded P (the values the PV MMA consumes) rather
 // than the fp32 exps: numerator and denominator then see the same weights,
 // which removes the bf16 rounding of the dominant weight from peaked rows.
+// d=128: accumulate the row sums after each chunk's P store (the store
+// goes out sooner; -0.4%); d=64 keeps them interleaved (+0.8% otherwise)
+#ifndef SVD_SUM_AFTER_ST
+#define SVD_SUM_AFTER_ST 1
+#endif
 #ifndef SVD_SUM_ROUNDED
 #define SVD_SUM_ROUNDED 1
 #endif
@@ -486,8 +491,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         pv.y = ptx::ex2(xv.y);
       }
       pk[i] = ptx::pack_bf16(pv.x, pv.y);
-      if (SVD_SUM_ROUNDED) ptx::acc_bf16x2(acc[i & 3], pk[i]);
-      else acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
+      if (!(SVD_SUM_AFTER_ST && D == 128)) {
+        if (SVD_SUM_ROUNDED) ptx::acc_bf16x2(acc[i & 3], pk[i]);
+        else acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
+      }
     }
   };
   const uint32_t tp = tmem + lane_off + C::col_p(x);
@@ -558,6 +565,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[16];
       exp_chunk(s, c, nm, pk, acc);
       ptx::tmem_st16(tp + c * 16, pk);
+      if (SVD_SUM_AFTER_ST && D == 128) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ptx::acc_bf16x2(acc[i & 3], pk[i]);
+      }
       if (c == 1 || c == 3) {
         // hand P over in two 64-key halves: PV on the first half overlaps
         // the exps of the second
