@@ -113,7 +113,9 @@ def main():
 def fit_points(points):
     """t = a + max(b * tiles, c * longest item's tiles) per head_dim: the
     fused launch is throughput-bound (all SMs busy) or bound by its longest
-    CTA (forced text/mixed query rows walk every key tile)."""
+    CTA (forced text/mixed query rows walk every key tile).  Fitted for the
+    smallest RMS relative error (sub-2 ms single-mode points are noisy on a
+    power-capped B200; a minimax fit lets them dominate)."""
     fit = {}
     for d in sorted({p["d"] for p in points}, reverse=True):
         pts = [p for p in points if p["d"] == d]
@@ -125,12 +127,13 @@ def fit_points(points):
             for b in np.linspace(0.5, 1.5, 101) * np.median(y / tiles):
                 feat = np.maximum(b * tiles, c * crit)
                 a = float(np.median(y - feat))
-                err = np.max(np.abs(a + feat - y) / y)
+                rel = (a + feat - y) / y
+                err = float(np.sqrt(np.mean(rel * rel)))
                 if best is None or err < best[0]:
-                    best = (err, a, b, c)
-        err, a, b, c = best
+                    best = (err, a, b, c, float(np.max(np.abs(rel))))
+        err, a, b, c, worst = best
         fit[d] = {"launch_ms": a, "ms_per_tile": float(b), "ms_per_critical_tile": float(c),
-                  "max_rel_err": float(err), "points": len(pts)}
+                  "rms_rel_err": err, "max_rel_err": worst, "points": len(pts)}
     return fit
 
 
