@@ -173,6 +173,15 @@ int svd_attn_fwd(const svd_plan* plan, const void* q, const void* k, const void*
                  const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
                  int32_t dtype, void* stream);
 
+/* As svd_attn_fwd, with an optional output head permutation: plan head h
+ * writes O head o_head_map[h] (device int32[n_heads]; NULL = identity).
+ * Lets a head-subset plan write straight into a full-layer O — e.g. pinned
+ * host memory, so the host-buffer pipeline needs no copy-out stage. */
+int svd_attn_fwd_ex(const svd_plan* plan, const void* q, const void* k, const void* v, void* o,
+                    const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                    const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                    int32_t dtype, const int32_t* o_head_map, void* stream);
+
 /* Fused compute + reassembly for multi-GPU: as svd_attn_fwd, but every
  * output row the plan (typically a svd_plan_shard view) produces is stored
  * into all n_peers O buffers — this rank's and its peers' [B, H, N,

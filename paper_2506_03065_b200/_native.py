@@ -106,6 +106,12 @@ SIGNATURES = {
          POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
          c_int32, c_int32, c_int32, c_int32, c_void_p],
     ),
+    "svd_attn_fwd_ex": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+         POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
+         c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p],
+    ),
     "svd_attn_fwd_peers": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,

@@ -173,12 +173,14 @@ class LayerPlan:
         return heads[: n.value], toks[: n.value]
 
     # -- execution
-    def forward(self, q, k, v, out, head_dim: int | None = None, stream=None) -> None:
+    def forward(self, q, k, v, out, head_dim: int | None = None, stream=None, o_head_map=None) -> None:
         """Launch the fused layer kernel on prepared bf16 CUDA tensors.
 
         q, k, v: [B, H, N, D] views with unit stride on D (D = 64 or 128);
         out: [B, H, N, D] (or the packed [rows, D] buffer of a shard plan).
         No host synchronisation; runs on `stream` (default: current stream).
+        o_head_map: optional device int32 [H] tensor — plan head h writes head
+        o_head_map[h] of `out` (a head-subset plan into a full-layer O).
         """
         import torch
 
@@ -193,10 +195,11 @@ class LayerPlan:
         else:
             ost = nat.i64x4(out.stride())
             batch = q.shape[0]
-        nat.check(nat.lib().svd_attn_fwd(
+        hmap = nat.c_void_p(o_head_map.data_ptr()) if o_head_map is not None else None
+        nat.check(nat.lib().svd_attn_fwd_ex(
             self._handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
             nat.c_void_p(v.data_ptr()), nat.c_void_p(out.data_ptr()), st[0], st[1], st[2], ost,
-            int(batch), hd, int(d_t), 0, nat.c_void_p(stream.cuda_stream)))
+            int(batch), hd, int(d_t), 0, hmap, nat.c_void_p(stream.cuda_stream)))
 
 
 def _device_sm_count() -> int:
@@ -295,6 +298,10 @@ def _to_device(xs):
 # boundaries come from a flow-shop model of the three stages (below).
 HOST_CHUNKS = int(__import__("os").environ.get("SVD_HOST_CHUNKS", "0"))
 PCIE_BYTES_PER_S = float(__import__("os").environ.get("SVD_PCIE_GBPS", "50")) * 1e9
+# opt-in: the kernel writes host-resident results straight into pinned memory
+# (no copy-out stage) — measured 1.8x SLOWER end to end on B200 / PCIe: the
+# epilogue's scattered 16-byte stores over PCIe stall the CTAs
+HOST_ZERO_COPY = __import__("os").environ.get("SVD_HOST_ZERO_COPY", "0") == "1"
 # Per-SM kernel time per KV step of a work item (two 128-row tiles x 128
 # keys), measured on B200 at power-capped clocks: HunyuanVideo 40.5 ms x 148
 # SMs / 2.89 M steps (d=128), CogVideoX 35.7 ms x 148 / 3.48 M (d=64); plus a
@@ -344,11 +351,12 @@ def _host_schedule(plan: LayerPlan, B: int, N: int, d: int):
     chunk starts the kernel early, a small last one shortens the drain)."""
     H = plan.n_heads
     cache = plan.__dict__.setdefault("_host_sched", {})
-    key = (B, N, d, HOST_CHUNKS)
+    key = (B, N, d, HOST_CHUNKS, HOST_ZERO_COPY)
     if key in cache:
         return cache[key]
     h2d = 3 * B * N * d * 2 / PCIE_BYTES_PER_S
-    d2h = B * N * d * 2 / PCIE_BYTES_PER_S
+    # zero-copy results leave with the kernel's own stores: no copy-out stage
+    d2h = 0.0 if (HOST_ZERO_COPY and _tensor_dim(d) == d) else B * N * d * 2 / PCIE_BYTES_PER_S
     if HOST_CHUNKS > 0:
         order = list(range(H))
         k = max(1, min(HOST_CHUNKS, H))
@@ -440,6 +448,18 @@ class _Staging:
         self.o = torch.empty((B, H, N, D), dtype=torch.bfloat16, device=dev)
         self.s_in, self.s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self.lock = threading.Lock()
+        self._maps = {}
+        self._dev = dev
+
+    def head_map(self, order, s0: int, s1: int):
+        """Device int32 tensor of the output heads of staging slots [s0, s1)."""
+        import torch
+
+        key = (tuple(order), s0, s1)
+        t = self._maps.get(key)
+        if t is None:
+            t = self._maps[key] = torch.tensor(order[s0:s1], dtype=torch.int32, device=self._dev)
+        return t
 
 
 def _host_staging(plan: "LayerPlan", dev, B: int, N: int, d: int, D: int) -> _Staging:
@@ -501,16 +521,26 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
                 ev = torch.cuda.Event()
                 ev.record(s_in)
                 loaded.append(ev)
+        # zero-copy result: the kernel stores rows straight into the pinned
+        # host O through a per-chunk head map (no copy-out stage to drain)
+        zero_copy = HOST_ZERO_COPY and D == d and out_host.is_pinned() and out_host.is_contiguous()
         computed = []
         for c in range(chunks):
             s0, s1 = bounds[c], bounds[c + 1]
             compute.wait_event(loaded[c])
             qc, kc, vc = (buf[:, s0:s1] for buf in st.qkv)
-            plan.heads_subplan(tuple(order[s0:s1])).forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d,
-                                                             stream=compute)
+            sub = plan.heads_subplan(tuple(order[s0:s1]))
+            if zero_copy:
+                sub.forward(qc, kc, vc, out_host, head_dim=d, stream=compute,
+                            o_head_map=st.head_map(order, s0, s1))
+            else:
+                sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=compute)
             ev = torch.cuda.Event()
             ev.record(compute)
             computed.append(ev)
+        if zero_copy:
+            compute.synchronize()
+            return out_host
         with torch.cuda.stream(s_out):
             for c in range(chunks):
                 s_out.wait_event(computed[c])

@@ -111,6 +111,8 @@ struct FwdParams {
   float* split_ml;
   int* split_tickets;
   int max_split_parts;
+  // optional output head permutation: plan head h writes O head o_head_map[h]
+  const int32_t* o_head_map;
 };
 
 // Store one 16-byte chunk of an output row: to o + off, or to every peer.
@@ -447,7 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.packed && p.n_peers == 0)
     orow = (int64_t(itp->out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
   else
-    orow = int64_t(b) * p.o_sb + int64_t(head) * p.o_sh + int64_t(tok_r) * p.o_sn;
+    orow = int64_t(b) * p.o_sb + int64_t(p.o_head_map ? __ldg(p.o_head_map + head) : head) * p.o_sh +
+           int64_t(tok_r) * p.o_sn;
 
   if (n_kv == 0) {
     // SKIP head (attention.py:51-54): exact zeros, no scores, no softmax
@@ -838,7 +841,8 @@ template <int D>
 static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const void* k,
                       const void* v, void* o, const int64_t* qs, const int64_t* ks,
                       const int64_t* vs, const int64_t* os, int32_t batch, int32_t head_dim,
-                      cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0) {
+                      cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0,
+                      const int32_t* o_head_map = nullptr) {
   using C = KCfg<D>;
   CUtensorMap mq, mk, mv;
   const int64_t N = P->grid.n, H = P->n_heads;
@@ -874,6 +878,7 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   prm.packed = P->sharded ? 1 : 0;
   prm.scale_log2 = float(1.4426950408889634 / std::sqrt(double(head_dim)));
   prm.n_peers = n_peers;
+  prm.o_head_map = o_head_map;
   if (P->n_split_groups > 0) {
     const size_t rows = size_t(P->n_split_groups) * size_t(P->max_split_parts) * 256;
     prm.split_o = static_cast<float*>(T->split_scratch);
@@ -902,16 +907,17 @@ extern "C" {
 
 const char* svd_version(void) { return "svdit_b200 0.1.0 sm_100a tcgen05/TMA"; }
 
-int svd_attn_fwd(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
-                 const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
-                 const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
-                 int32_t dtype, void* stream) {
+int svd_attn_fwd_ex(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
+                    const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                    const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                    int32_t dtype, const int32_t* o_head_map, void* stream) {
   if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
   if (dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
   if (head_dim < 1 || head_dim > tensor_dim)
     return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
   if (batch < 1) return fail(SVD_ERR_SHAPE, "batch must be >= 1");
   if (P->sharded && batch != 1) return fail(SVD_ERR_UNSUPPORTED, "shard plans run with batch 1");
+  if (P->sharded && o_head_map) return fail(SVD_ERR_UNSUPPORTED, "shard plans write packed rows");
   if (!q || !k || !v || !o) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
   if (o_strides[3] != 1 || (o_strides[2] * 2) % 16 != 0 ||
       (reinterpret_cast<uintptr_t>(o) & 15) != 0)
@@ -923,14 +929,22 @@ int svd_attn_fwd(const svd_plan* P, const void* q, const void* k, const void* v,
   switch (tensor_dim) {
     case 64:
       return launch_fwd<64>(P, T, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch,
-                            head_dim, s);
+                            head_dim, s, nullptr, 0, o_head_map);
     case 128:
       return launch_fwd<128>(P, T, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch,
-                             head_dim, s);
+                             head_dim, s, nullptr, 0, o_head_map);
     default:
       return fail(SVD_ERR_UNSUPPORTED,
                   "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
   }
+}
+
+int svd_attn_fwd(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
+                 const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                 const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                 int32_t dtype, void* stream) {
+  return svd_attn_fwd_ex(P, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch, head_dim,
+                         tensor_dim, dtype, nullptr, stream);
 }
 
 #ifdef SVD_TRACE

@@ -61,3 +61,32 @@ def test_out_buffer_host_and_device(d):
     assert got.data_ptr() == dout.data_ptr() and torch.equal(dout.cpu(), want)
     with pytest.raises(S.ShapeError):
         S.fused_layer_attention(q, k, v, groups, out=torch.empty(1, 3, 1024, d))
+
+
+def test_output_head_map_and_zero_copy(monkeypatch):
+    """svd_attn_fwd_ex's output head map (a head-subset plan writing into a
+    full-layer O) and the opt-in zero-copy host pipeline give the same bits."""
+    import torch
+
+    from paper_2506_03065_b200 import attention as A
+
+    g = S.block_grid(S.TokenLayout(0, 8, 128, 64))
+    specs = [S.diagonal_spec(1), S.full_spec(), S.skip_spec(), S.multi_diagonal_spec()]
+    plan = S.plan_for_assignment(specs, S.TokenLayout(0, 8, 128, 64))
+    q, k, v = (torch.randn(1, 4, 1024, 64, device="cuda").to(torch.bfloat16) for _ in range(3))
+    ref = torch.empty_like(q)
+    plan.forward(q, k, v, ref)
+    heads = (3, 1)
+    sub = plan.heads_subplan(heads)
+    out = torch.zeros_like(q)
+    sub.forward(q[:, list(heads)].contiguous(), k[:, list(heads)].contiguous(), v[:, list(heads)].contiguous(),
+                out, o_head_map=torch.tensor(heads, dtype=torch.int32, device="cuda"))
+    for h in heads:
+        assert torch.equal(out[:, h], ref[:, h])
+    assert not out[:, 0].any() and not out[:, 2].any()
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    groups = S.group_heads(specs, g)
+    want = S.fused_layer_attention(hq, hk, hv, groups)
+    monkeypatch.setattr(A, "HOST_ZERO_COPY", True)
+    got = S.fused_layer_attention(hq, hk, hv, groups)
+    assert torch.equal(got, want) and torch.equal(got, ref.cpu())
