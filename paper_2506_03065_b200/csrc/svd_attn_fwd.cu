@@ -11,15 +11,18 @@
 // CTA anatomy (384 threads, 1 CTA / SM):
 //   warp 0       TMA producer: Q tiles once, then K and V tiles through two
 //                separate smem rings (SWIZZLE_128B boxes of 64x64 bf16)
-//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 1       TMEM allocator + tcgen05.mma issuer (d=128: the whole warp,
+//                one elected lane per MMA; d=64: lane 0)
 //   warps 4-7    softmax/epilogue for Q tile A (thread = row = TMEM lane)
 //   warps 8-11   softmax/epilogue for Q tile B
 // Per KV tile j the issuer runs, ping-ponging between the two Q tiles,
 //   S_X = Q_X K_j^T          (SS MMA, M=128 N=128 K=d, fp32 in TMEM)
 //   O_X += P_X V_j           (TS MMA: P bf16 from TMEM, V MN-major in smem)
 // while the softmax warpgroups turn S_X into P_X (masking, running max with
-// lazy rescale of O, exp2, row sums) — so one tile's exp overlaps the other
-// tile's MMAs.
+// lazy rescale of O, exp2 — at d=128 3/8 of it on the FMA pipe — bf16 P,
+// rounded row sums) — so one tile's exps overlap the other tile's MMAs.
+// Split-KV items (shard plans) publish partial (m, l, O) and the last part
+// merges; the epilogue can store into several ranks' O (peer memory).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
