@@ -16,6 +16,7 @@
  *   attention.py:57-98  sparse_attention(q,k,v,mask)   svd_plan_create_from_masks + svd_attn_fwd
  *   attention.py:101-105 full_mask_attention(...)      svd_plan_create (FULL spec) + svd_attn_fwd
  *   attention.py:51-54  skip_attention(...)            svd_plan_create (SKIP spec) + svd_attn_fwd
+ *   attention.py:108-146 block_key_mass(q, k, grid)    svd_block_key_mass
  *   model.py:352-355    _layernorm (layer_qkv / layer_finish)   svd_layernorm
  *   model.py:169-195    rope(q), rope(k) (layer_qkv)            svd_rope_table + svd_rope_apply
  *   model.py:357-359    _gelu (layer_finish MLP)                svd_gelu
@@ -210,6 +211,19 @@ int svd_ipc_close(void* ptr, int64_t offset);
 int svd_head_sqdiff(const void* a, const void* b, const int64_t* a_strides,
                     const int64_t* b_strides, int32_t batch, int32_t heads, int64_t n_tokens,
                     int32_t head_dim, double* out, void* stream);
+
+/* ---- block_key_mass (attention.py:108-146; the search's stripe calibration) --
+ * mass[b, h, kb] (device double [B, H, nb], nb = ceil(N / block_size)) = the
+ * softmax attention mass of all query rows on key block kb, / N: each (b, h)
+ * row sums to 1.  q, k: bf16 [B, H, N, tensor_dim] via element strides,
+ * scale 1/sqrt(head_dim).  Two tensor-core passes (row max / sum, then
+ * per-key sums) and an fp64 per-block sum; deterministic.  workspace: device
+ * scratch of svd_key_mass_workspace(batch, heads, N) bytes, 16-byte aligned. */
+int64_t svd_key_mass_workspace(int32_t batch, int32_t heads, int64_t n_tokens);
+int svd_block_key_mass(const void* q, const void* k, const int64_t* q_strides,
+                       const int64_t* k_strides, int32_t batch, int32_t heads, int64_t n_tokens,
+                       int32_t head_dim, int32_t tensor_dim, int32_t block_size, int32_t dtype,
+                       void* workspace, int64_t workspace_bytes, double* mass, void* stream);
 
 /* Scatter a gathered [world * max_rows, d] buffer of packed shard rows back
  * into O [B=1, H, N, d] (the multi-GPU reassembly after the NCCL all-gather). */

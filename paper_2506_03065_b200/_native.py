@@ -130,6 +130,12 @@ SIGNATURES = {
         c_int,
         [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, POINTER(c_int64), c_int32, c_void_p],
     ),
+    "svd_key_mass_workspace": (c_int64, [c_int32, c_int32, c_int64]),
+    "svd_block_key_mass": (
+        c_int,
+        [c_void_p, c_void_p, POINTER(c_int64), POINTER(c_int64), c_int32, c_int32, c_int64, c_int32,
+         c_int32, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_void_p],
+    ),
     "svd_layernorm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, ctypes.c_float,
                               c_void_p]),
     "svd_rope_table": (c_int, [c_void_p, c_int64, c_int32, c_double, c_void_p]),

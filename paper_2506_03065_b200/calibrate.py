@@ -11,9 +11,8 @@ mode_loss and select_mode; stripe columns from block_key_mass
 Everything runs through the fused sm_100a layer kernel: each candidate is one
 launch of the plan for that candidate's per-head specs (the sparse
 candidates cost ~3-5% of FULL each), the per-head MSE is an fp64 device
-reduction (svd_head_sqdiff), and block_key_mass reuses the same kernel with
-one-hot value columns (O[r, j] = sum of normalised attention of row r over
-key block j).
+reduction (svd_head_sqdiff), and block_key_mass is its own two-pass
+tensor-core kernel (csrc/svd_key_mass.cu).
 """
 
 from __future__ import annotations
@@ -47,8 +46,9 @@ def head_sqdiff(a, b=None):
 def block_key_mass(q, k, grid: BlockGrid):
     """Per-head attention mass on each key block, [B, H, nb], summing to 1 per
     (batch, head) (attention.py:108-146).  NumPy inputs give a float64 NumPy
-    result; CUDA tensors a float32 CUDA tensor.  Computed as FULL attention
-    with one-hot value columns, nb/D launches (D = 64 or 128)."""
+    result; CUDA tensors a float64 CUDA tensor.  Computed by
+    svd_block_key_mass (csrc/svd_key_mass.cu): a row-statistics pass and a
+    per-key-sum pass of QK^T on the tensor cores, then an fp64 block sum."""
     import torch
 
     for name, t in (("q", q), ("k", k)):
@@ -63,23 +63,32 @@ def block_key_mass(q, k, grid: BlockGrid):
     (qt, kt), was_numpy, dev = _to_device((q, k))
     D = qt.shape[-1]
     nb = grid.n_blocks
-    plan = plan_for_assignment([full_spec()] * H, grid.layout)
-    blk = torch.as_tensor(np.repeat(np.arange(nb), np.diff(grid.bounds)), device=dev)
-    mass = torch.empty(B, H, nb, dtype=torch.float32, device=dev)
-    out = torch.empty(B, H, N, D, dtype=torch.bfloat16, device=dev)
-    tok = torch.arange(N, device=dev)
-    for c0 in range(0, nb, D):
-        cols = min(D, nb - c0)
-        onehot = torch.zeros(N, D, dtype=torch.bfloat16, device=dev)
-        sel = (blk >= c0) & (blk < c0 + cols)
-        onehot[tok[sel], blk[sel] - c0] = 1.0
-        vt = onehot.expand(B, H, N, D).contiguous()
-        plan.forward(qt, kt, vt, out, head_dim=d)
-        mass[:, :, c0:c0 + cols] = out[..., :cols].float().sum(dim=2)
-    mass /= N
+    lib = nat.lib()
+    ws_bytes = int(lib.svd_key_mass_workspace(B, H, N))
+    ws = _workspace(dev, ws_bytes)
+    mass = torch.empty(B, H, nb, dtype=torch.float64, device=dev)
+    nat.check(lib.svd_block_key_mass(
+        nat.c_void_p(qt.data_ptr()), nat.c_void_p(kt.data_ptr()), nat.i64x4(qt.stride()),
+        nat.i64x4(kt.stride()), B, H, N, d, D, int(grid.layout.block_size), 0,
+        nat.c_void_p(ws.data_ptr()), ws_bytes, nat.c_void_p(mass.data_ptr()),
+        nat.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
     if was_numpy:
-        return mass.double().cpu().numpy()
+        return mass.cpu().numpy()
     return mass
+
+
+_WORKSPACES: dict = {}
+
+
+def _workspace(dev, nbytes: int):
+    """A per-device scratch buffer of at least nbytes (grown, never shrunk)."""
+    import torch
+
+    key = dev.index
+    buf = _WORKSPACES.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = _WORKSPACES[key] = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    return buf
 
 
 def top_stripes(mass_row: np.ndarray, count: int) -> tuple[int, ...]:

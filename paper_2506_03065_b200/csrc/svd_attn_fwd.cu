@@ -757,7 +757,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-static int make_tmap(CUtensorMap* map, const void* ptr, const int64_t* st, int64_t B, int64_t H,
+// shared with svd_key_mass.cu
+int make_tmap(CUtensorMap* map, const void* ptr, const int64_t* st, int64_t B, int64_t H,
                      int64_t N, int D, const char* name) {
   auto enc = get_encode_fn();
   if (!enc) return fail(SVD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");

@@ -13,8 +13,8 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 
-def _inputs(seed, h, n, d, qscale=2.0):
-    q, k, v = O.random_qkv(seed, 1, h, n, d)
+def _inputs(seed, h, n, d, qscale=2.0, b=1):
+    q, k, v = O.random_qkv(seed, b, h, n, d)
     return O.bf16_round(q * np.float32(qscale)), O.bf16_round(k), O.bf16_round(v)
 
 
@@ -28,8 +28,10 @@ def test_block_key_mass_golden(golden_attn):
         got = S.block_key_mass(q, k, g)
         want = golden_attn[f"bkm{bi}_out"]
         assert got.shape == want.shape
-        np.testing.assert_allclose(got, want, rtol=0, atol=2e-3)
-        np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=5e-3)
+        # fp32 scores of the same bf16 inputs vs the reference's fp64: the
+        # masses agree far inside bf16 resolution
+        np.testing.assert_allclose(got, want, rtol=0, atol=2e-5)
+        np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=1e-5)
 
 
 @pytest.mark.parametrize("lay,d", [((96, 16, 250, 64), 128), ((0, 16, 256, 64), 64)])
@@ -38,14 +40,48 @@ def test_block_key_mass_vs_oracle_and_topk(lay, d):
     q, k, _ = _inputs(5, 3, og.n, d, 3.0)
     want = O.block_key_mass(q, k, og)
     got = S.block_key_mass(q, k, S.block_grid(S.TokenLayout(*lay)))
-    np.testing.assert_allclose(got, want, rtol=0, atol=2e-3)
+    np.testing.assert_allclose(got, want, rtol=0, atol=2e-5)
     from paper_2506_03065_b200.calibrate import top_stripes
 
     for h in range(3):
         a, b = top_stripes(got[0, h], 2), top_stripes(want[0, h], 2)
         order = np.sort(want[0, h])[::-1]
-        if order[1] - order[2] > 5e-3:  # clear margin: selection must agree
+        if order[1] - order[2] > 1e-4:  # clear margin: selection must agree
             assert a == b
+
+
+@pytest.mark.parametrize("lay,h,d,b", [
+    ((0, 1, 40, 16), 2, 64, 1),       # N = 40 < one 64-row segment
+    ((5, 3, 100, 48), 3, 128, 2),     # block 48 (not a multiple of 64), batch 2
+    ((70, 4, 300, 100), 2, 32, 1),    # block 100 straddles 128-key tiles; d padded 32 -> 64
+    ((0, 2, 128, 128), 2, 128, 1),    # N = 256: exact tiles, block 128
+    ((13, 5, 211, 64), 1, 96, 1),     # ragged tail, d 96 -> 128
+])
+def test_block_key_mass_edges(lay, h, d, b):
+    og = O.block_grid(*lay)
+    q, k, _ = _inputs(7, h, og.n, d, 3.0, b)
+    want = O.block_key_mass(q, k, og)
+    got = S.block_key_mass(q, k, S.block_grid(S.TokenLayout(*lay)))
+    assert got.shape == want.shape == (b, h, len(og.bounds) - 1)
+    np.testing.assert_allclose(got, want, rtol=0, atol=2e-5)
+    np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=1e-5)
+
+
+def test_block_key_mass_strided_and_deterministic():
+    """[B, N, H, d] storage runs without copies; repeated calls are bit-identical."""
+    import torch
+
+    lay = (96, 8, 250, 64)
+    og = O.block_grid(*lay)
+    g = S.block_grid(S.TokenLayout(*lay))
+    q, k, _ = _inputs(3, 4, og.n, 128, 3.0)
+    qs = torch.from_numpy(np.ascontiguousarray(q.transpose(0, 2, 1, 3))).cuda().bfloat16().permute(0, 2, 1, 3)
+    ks = torch.from_numpy(np.ascontiguousarray(k.transpose(0, 2, 1, 3))).cuda().bfloat16().permute(0, 2, 1, 3)
+    a = S.block_key_mass(qs, ks, g)
+    b = S.block_key_mass(qs, ks, g)
+    assert a.dtype == torch.float64 and a.is_cuda
+    assert torch.equal(a, b)
+    np.testing.assert_allclose(a.cpu().numpy(), O.block_key_mass(q, k, og), rtol=0, atol=2e-5)
 
 
 def test_head_sqdiff_matches_fp64():
