@@ -85,3 +85,25 @@ def test_random_layers_vs_oracle(seed):
         done += 1
     assert done >= 18
     print(f"seed {seed}: {done} cases, worst max-abs {worst:.3e}")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_block_key_mass_vs_oracle(seed):
+    """block_key_mass (attention.py:108-146) on random layouts / block sizes /
+    head dims / batches / storage orders vs the fp64 oracle."""
+    import torch
+
+    rng = np.random.default_rng(777 + seed)
+    for case in range(10):
+        lay, specs, d, B, qscale = _random_case(rng)
+        og = O.block_grid(*lay)
+        H = min(len(specs), 3)
+        q, k, _ = O.random_qkv(90 + case, B, H, og.n, d)
+        q, k = O.bf16_round(q * np.float32(qscale)), O.bf16_round(k)
+        want = O.block_key_mass(q, k, og)
+        tq, tk = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k))
+        if case % 2:
+            tq, tk = (t.transpose(1, 2).contiguous().transpose(1, 2) for t in (tq, tk))
+        got = S.block_key_mass(tq, tk, S.block_grid(S.TokenLayout(*lay))).cpu().numpy()
+        np.testing.assert_allclose(got, want, rtol=0, atol=2e-5, err_msg=str((case, lay, d, B, qscale)))
+        np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=1e-5)
