@@ -407,6 +407,10 @@ def run_ours(args):
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    # bytes copied per step: one GPU pipelines every non-SKIP head's Q/K/V in and
+    # O out; a shard rank copies the full Q/K/V in and the full O out
+    e2e_bytes = (S.host_transfer_bytes(plan, 1, n, d) if world == 1
+                 else (3 * H * n * d * 2, H * n * d * 2))
     if world > 1:
         import torch.distributed as dist
 
@@ -490,10 +494,11 @@ def run_ours(args):
             "unit": "TFLOP/s (effective, dense-equivalent)",
             "ms_per_layer": round(e2e_ms, 3),
             "wall_ms_steps": e2e_walls,
-            "h2d_bytes_per_step": 3 * H * n * d * 2,
-            "d2h_bytes_per_step": H * n * d * 2,
+            "h2d_bytes_per_step": e2e_bytes[0],
+            "d2h_bytes_per_step": e2e_bytes[1],
             "path": ("fused_layer_attention(pinned host bf16 Q/K/V, out=pinned O): heads reordered and "
-                     "chunked by a flow-shop model, H2D / kernel / D2H streams overlapped"),
+                     "chunked by a flow-shop model, H2D / kernel / D2H streams overlapped; SKIP heads "
+                     "never cross PCIe (zeros written on the host)"),
         },
         "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),
         "clocks": clock,

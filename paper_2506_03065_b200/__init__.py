@@ -45,6 +45,7 @@ from .attention import (
     full_mask_attention,
     fused_layer_attention,
     group_heads,
+    host_transfer_bytes,
     plan_for_assignment,
     skip_attention,
     sparse_attention,

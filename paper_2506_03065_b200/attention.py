@@ -121,6 +121,18 @@ class LayerPlan:
                                                  nat.ctypes.byref(n), nat.ctypes.byref(skip)))
         return tuple(int(h) for h in heads), bool(skip.value)
 
+    def skip_heads(self) -> tuple[int, ...]:
+        """Heads of SKIP groups (exact zeros: no inputs read, no kernel work)."""
+        cache = self.__dict__.setdefault("_skip_heads", [])
+        if not cache:
+            hs = []
+            for g in range(self.info.n_groups):
+                heads, skip = self.group_heads(g)
+                if skip:
+                    hs.extend(heads)
+            cache.append(tuple(sorted(hs)))
+        return cache[0]
+
     def group_mask(self, g: int) -> np.ndarray:
         nb = self.layout.n_blocks
         active = np.empty((nb, nb), dtype=np.uint8)
@@ -302,6 +314,8 @@ PCIE_BYTES_PER_S = float(__import__("os").environ.get("SVD_PCIE_GBPS", "50")) * 
 # (no copy-out stage) — measured 1.8x SLOWER end to end on B200 / PCIe: the
 # epilogue's scattered 16-byte stores over PCIe stall the CTAs
 HOST_ZERO_COPY = __import__("os").environ.get("SVD_HOST_ZERO_COPY", "0") == "1"
+# consecutive chunk kernels on two alternating streams (SVD_HOST_OVERLAP=0: one)
+HOST_OVERLAP = __import__("os").environ.get("SVD_HOST_OVERLAP", "1") == "1"
 # Per-SM kernel time per KV step of a work item (two 128-row tiles x 128
 # keys), measured on B200 at power-capped clocks: HunyuanVideo 40.5 ms x 148
 # SMs / 2.89 M steps (d=128), CogVideoX 35.7 ms x 148 / 3.48 M (d=64); plus a
@@ -313,14 +327,24 @@ LAUNCH_SECONDS = 15e-6
 
 def _flow_shop(bounds, h2d, kernel, d2h) -> float:
     """Makespan of chunks [bounds[i], bounds[i+1]) of a head order through
-    three in-order stages (H2D stream, compute stream, D2H stream; PCIe is
-    full duplex).  kernel(a, b): modelled launch time of order[a:b]."""
+    three in-order stages (H2D stream, compute, D2H stream; PCIe is full
+    duplex).  kernel(a, b) -> (SM-throughput time, longest item) of the launch
+    of order[a:b].  Consecutive launches overlap (two compute streams,
+    HOST_OVERLAP): a launch holds the SMs for its throughput time, and its
+    output is complete once its longest item is too; with one stream a
+    launch occupies the GPU for max(throughput, longest)."""
     t1 = t2 = t3 = 0.0
     for c in range(len(bounds) - 1):
         a, b = bounds[c], bounds[c + 1]
         t1 += h2d * (b - a)
-        t2 = max(t2, t1) + kernel(a, b)
-        t3 = max(t3, t2) + d2h * (b - a)
+        thr, longest = kernel(a, b)
+        start = max(t2, t1)
+        if HOST_OVERLAP:
+            t2 = start + thr
+            done = max(t2, start + longest) + LAUNCH_SECONDS
+        else:
+            t2 = done = start + max(thr, longest) + LAUNCH_SECONDS
+        t3 = max(t3, done) + d2h * (b - a)
     return t3
 
 
@@ -349,24 +373,29 @@ def _host_schedule(plan: LayerPlan, B: int, N: int, d: int):
     the light heads hide under it; then the rest by falling kernel time), and
     the chunk boundaries by local search from equal chunks (a small first
     chunk starts the kernel early, a small last one shortens the drain)."""
-    H = plan.n_heads
+    skip = set(plan.skip_heads())
+    active = [h for h in range(plan.n_heads) if h not in skip]  # SKIP heads never cross PCIe
+    H = len(active)
     cache = plan.__dict__.setdefault("_host_sched", {})
     key = (B, N, d, HOST_CHUNKS, HOST_ZERO_COPY)
     if key in cache:
+        return cache[key]
+    if H == 0:
+        cache[key] = ([], [0])
         return cache[key]
     h2d = 3 * B * N * d * 2 / PCIE_BYTES_PER_S
     # zero-copy results leave with the kernel's own stores: no copy-out stage
     d2h = 0.0 if (HOST_ZERO_COPY and _tensor_dim(d) == d) else B * N * d * 2 / PCIE_BYTES_PER_S
     if HOST_CHUNKS > 0:
-        order = list(range(H))
+        order = list(active)
         k = max(1, min(HOST_CHUNKS, H))
         bounds = [round(i * H / k) for i in range(k + 1)]
     else:
         work, longest = _launch_model(plan, B, d)
         sms = _device_sm_count()
         solo = [max(w / sms, t) for w, t in zip(work, longest)]
-        heavy = sorted((h for h in range(H) if solo[h] >= h2d), key=lambda h: (-solo[h], h))
-        light = sorted((h for h in range(H) if solo[h] < h2d), key=lambda h: (-solo[h], h))
+        heavy = sorted((h for h in active if solo[h] >= h2d), key=lambda h: (-solo[h], h))
+        light = sorted((h for h in active if solo[h] < h2d), key=lambda h: (-solo[h], h))
         hpre = {}
 
         def cost(o, bd):
@@ -375,7 +404,7 @@ def _host_schedule(plan: LayerPlan, B: int, N: int, d: int):
                 wp.append(wp[-1] + work[h])
 
             def kernel(a, b):
-                return max((wp[b] - wp[a]) / sms, max(longest[h] for h in o[a:b])) + LAUNCH_SECONDS
+                return (wp[b] - wp[a]) / sms, max(longest[h] for h in o[a:b])
 
             return _flow_shop(bd, h2d, kernel, d2h)
 
@@ -401,7 +430,7 @@ def _host_schedule(plan: LayerPlan, B: int, N: int, d: int):
             return bd, c0
 
         best_all = None
-        for cand_order in (heavy + light, list(range(H))):  # Johnson's order, the given order
+        for cand_order in (heavy + light, list(active)):  # Johnson's order, the given order
             bd, c0 = None, float("inf")
             for k in range(1, min(H, 12) + 1):
                 nb = [round(i * H / k) for i in range(k + 1)]
@@ -447,6 +476,9 @@ class _Staging:
         self.qkv = [torch.zeros((B, H, N, D), dtype=torch.bfloat16, device=dev) for _ in range(3)]
         self.o = torch.empty((B, H, N, D), dtype=torch.bfloat16, device=dev)
         self.s_in, self.s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        # chunk kernels alternate between the caller's stream and this one, so
+        # the next chunk's CTAs fill the SMs the previous chunk's tail frees
+        self.s_comp = torch.cuda.Stream(dev)
         self.lock = threading.Lock()
         self._maps = {}
         self._dev = dev
@@ -501,6 +533,10 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
     else:
         _check_out(out, (B, H, N, d), "cpu")
         out_host = out
+    skip = plan.skip_heads()
+    if chunks == 0:  # every head SKIP
+        out_host.zero_()
+        return out_host
     # staging slot s holds head order[s]; chunks are contiguous slot ranges
     st = _host_staging(plan, dev, B, N, d, D)
     with st.lock:
@@ -525,29 +561,44 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
         # host O through a per-chunk head map (no copy-out stage to drain)
         zero_copy = HOST_ZERO_COPY and D == d and out_host.is_pinned() and out_host.is_contiguous()
         computed = []
+        streams = (compute, st.s_comp) if HOST_OVERLAP else (compute,)
+        st.s_comp.wait_stream(compute)  # the caller's prior work on its stream
         for c in range(chunks):
             s0, s1 = bounds[c], bounds[c + 1]
-            compute.wait_event(loaded[c])
+            cs = streams[c % len(streams)]
+            cs.wait_event(loaded[c])
             qc, kc, vc = (buf[:, s0:s1] for buf in st.qkv)
             sub = plan.heads_subplan(tuple(order[s0:s1]))
             if zero_copy:
-                sub.forward(qc, kc, vc, out_host, head_dim=d, stream=compute,
+                sub.forward(qc, kc, vc, out_host, head_dim=d, stream=cs,
                             o_head_map=st.head_map(order, s0, s1))
             else:
-                sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=compute)
+                sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=cs)
             ev = torch.cuda.Event()
-            ev.record(compute)
+            ev.record(cs)
             computed.append(ev)
+        if len(streams) > 1:
+            compute.wait_stream(st.s_comp)  # the caller's stream sees every chunk
+        with torch.cuda.stream(s_out):
+            if not zero_copy:
+                for c in range(chunks):
+                    s_out.wait_event(computed[c])
+                    for slot in range(bounds[c], bounds[c + 1]):
+                        out_host[:, order[slot]].copy_(st.o[:, slot, :, :d], non_blocking=True)
+        for h in skip:  # SKIP heads (attention.py:51-54): zeros written on the host, under the GPU work
+            out_host[:, h].zero_()
         if zero_copy:
             compute.synchronize()
-            return out_host
-        with torch.cuda.stream(s_out):
-            for c in range(chunks):
-                s_out.wait_event(computed[c])
-                for slot in range(bounds[c], bounds[c + 1]):
-                    out_host[:, order[slot]].copy_(st.o[:, slot, :, :d], non_blocking=True)
-        s_out.synchronize()  # a host result must be readable on return
+        else:
+            s_out.synchronize()  # a host result must be readable on return
     return out_host
+
+
+def host_transfer_bytes(plan: LayerPlan, B: int, N: int, d: int) -> tuple[int, int]:
+    """(H2D, D2H) bytes one host-buffer call moves: bf16 Q/K/V in and O out
+    for every head except SKIP heads (their zeros are written on the host)."""
+    h = plan.n_heads - len(plan.skip_heads())
+    return 3 * B * h * N * d * 2, B * h * N * d * 2
 
 
 def _run(plan: LayerPlan, q, k, v, out=None):
@@ -743,6 +794,6 @@ def block_key_mass(q, k, grid: BlockGrid):
 
 
 __all__ = [
-    "LayerPlan", "HeadGroup", "group_heads", "fused_layer_attention", "sparse_attention", "block_key_mass",
+    "LayerPlan", "HeadGroup", "group_heads", "host_transfer_bytes", "fused_layer_attention", "sparse_attention", "block_key_mass",
     "full_mask_attention", "dense_attention", "skip_attention", "plan_for_assignment",
 ]

@@ -128,19 +128,26 @@ def test_host_pipeline_schedule_is_a_partition_and_beats_equal_chunks():
     plan = S.plan_for_assignment(asg, layout)
     H, N, d = len(asg), layout.total_tokens, 128
     order, bounds = A._host_schedule(plan, 1, N, d)
-    assert sorted(order) == list(range(H))
-    assert bounds[0] == 0 and bounds[-1] == H and all(a < b for a, b in zip(bounds, bounds[1:]))
+    skip = asg.index(S.skip_spec())
+    assert plan.skip_heads() == (skip,)
+    # SKIP heads never cross PCIe: the order is a permutation of the other heads
+    assert sorted(order) == [h for h in range(H) if h != skip]
+    assert S.host_transfer_bytes(plan, 1, N, d) == (3 * (H - 1) * N * d * 2, (H - 1) * N * d * 2)
+    assert bounds[0] == 0 and bounds[-1] == H - 1 and all(a < b for a, b in zip(bounds, bounds[1:]))
     work, longest = A._launch_model(plan, 1, d)
     sms = A._device_sm_count()
     h2d, d2h = 3 * N * d * 2 / A.PCIE_BYTES_PER_S, N * d * 2 / A.PCIE_BYTES_PER_S
 
     def makespan(o, bd):
         def kernel(a, b):
-            return max(sum(work[h] for h in o[a:b]) / sms, max(longest[h] for h in o[a:b])) + A.LAUNCH_SECONDS
+            return sum(work[h] for h in o[a:b]) / sms, max(longest[h] for h in o[a:b])
         return A._flow_shop(bd, h2d, kernel, d2h)
 
-    equal = [round(i * H / 6) for i in range(7)]
-    assert makespan(order, bounds) <= makespan(list(range(H)), equal) + 1e-9
+    rest = [h for h in range(H) if h != skip]
+    equal = [round(i * len(rest) / 6) for i in range(7)]
+    assert makespan(order, bounds) <= makespan(rest, equal) + 1e-9
+    all_skip = S.plan_for_assignment([S.skip_spec()] * 3, layout)
+    assert A._host_schedule(all_skip, 1, N, d) == ([], [0])
     # sub-plans of a head subset keep each head's schedule: same work as the full plan
     assert sum(plan.heads_subplan((h,)).info.computed_tiles for h in range(H)) == plan.info.computed_tiles
 

@@ -63,6 +63,18 @@ def test_out_buffer_host_and_device(d):
         S.fused_layer_attention(q, k, v, groups, out=torch.empty(1, 3, 1024, d))
 
 
+def test_host_all_skip_layer():
+    """Every head SKIP: nothing crosses PCIe, the host O is zeroed in place."""
+    import torch
+
+    g = S.block_grid(S.TokenLayout(0, 8, 128, 64))
+    groups = S.group_heads([S.skip_spec()] * 2, g)
+    q, k, v = (torch.randn(1, 2, 1024, 64).to(torch.bfloat16).pin_memory() for _ in range(3))
+    hout = torch.full(q.shape, 7.0, dtype=torch.bfloat16).pin_memory()
+    got = S.fused_layer_attention(q, k, v, groups, out=hout)
+    assert got.data_ptr() == hout.data_ptr() and not hout.any()
+
+
 def test_output_head_map_and_zero_copy(monkeypatch):
     """svd_attn_fwd_ex's output head map (a head-subset plan writing into a
     full-layer O) and the opt-in zero-copy host pipeline give the same bits."""
