@@ -136,10 +136,17 @@ class CandidateEvaluator:
         return self._s_stripe[cols]
 
     def resolve_stripes(self, q, k, heads) -> dict:
-        """Stripe columns for the listed heads from block_key_mass (batch 0)."""
+        """Stripe columns for the listed heads from block_key_mass (batch 0;
+        search.py:340-346).  Heads are independent, so only the listed heads'
+        masses are computed."""
+        heads = list(heads)
+        if not heads:
+            return {}
+        if len(heads) < q.shape[1]:
+            q, k = q[:, heads], k[:, heads]
         mass = block_key_mass(q, k, self.grid)
         m0 = mass[0].double().cpu().numpy() if _is_torch(mass) else mass[0]
-        return {h: top_stripes(m0[h], self.params.patterns.stripe_count) for h in heads}
+        return {h: top_stripes(m0[i], self.params.patterns.stripe_count) for i, h in enumerate(heads)}
 
     def evaluate(self, q, k, v, stripes: dict | None = None) -> LayerEvaluation:
         import torch

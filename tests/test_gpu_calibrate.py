@@ -134,3 +134,25 @@ def test_candidate_evaluator_vs_oracle():
     for h, ch in enumerate(res.choices):
         if ch is S.Mode.SKIP:
             assert not sel[:, h].any()
+
+
+def test_resolve_stripes_head_subset():
+    """Stripe columns for a head subset equal the full-layer selection's
+    (search.py:340-346 computes the mass of every head, then keeps the
+    unresolved ones)."""
+    from paper_2506_03065_b200.calibrate import CandidateEvaluator, top_stripes
+
+    lay = (96, 16, 250, 64)
+    og = O.block_grid(*lay)
+    g = S.block_grid(S.TokenLayout(*lay))
+    q, k, _ = _inputs(13, 5, og.n, 64, 3.0)
+    ev = CandidateEvaluator(g, S.SearchParams())
+    full = ev.resolve_stripes(q, k, range(5))
+    sub = ev.resolve_stripes(q, k, [3, 1])
+    assert sub == {3: full[3], 1: full[1]}
+    want = O.block_key_mass(q, k, og)[0]
+    for h in range(5):
+        order = np.sort(want[h])[::-1]
+        if order[1] - order[2] > 1e-4:
+            assert full[h] == top_stripes(want[h], 2)
+    assert ev.resolve_stripes(q, k, []) == {}
