@@ -56,3 +56,27 @@ def test_plan_create_from_masks_rejects_empty_row():
     m[2, 2] = False
     with pytest.raises(S.DegenerateRowError):
         S.LayerPlan.from_masks(layout, [m], [0])
+
+
+def test_block_key_mass_argument_checks_without_a_gpu():
+    """svd_block_key_mass validates its arguments before touching the device;
+    svd_key_mass_workspace sizes (-m, 1/l) rows + fp64 key sums per 128-token tile."""
+    lib = nat.lib()
+    assert lib.svd_key_mass_workspace(1, 24, 119056) == 24 * 931 * (256 * 4 + 128 * 8)
+    assert lib.svd_key_mass_workspace(0, 1, 1) == 0
+    st = nat.i64x4((128, 128, 128, 1))
+    dummy = ctypes.c_void_p(16)
+
+    def call(q=dummy, k=dummy, batch=1, heads=1, n=128, head_dim=64, tensor_dim=64, block=64, dtype=0,
+             ws=dummy, ws_bytes=1 << 20, mass=dummy):
+        return lib.svd_block_key_mass(q, k, st, st, batch, heads, n, head_dim, tensor_dim, block, dtype,
+                                      ws, ws_bytes, mass, None)
+
+    assert call(q=None) == 4                      # NULL tensor -> ConfigError
+    assert call(dtype=1) == 6                     # fp16 unsupported
+    assert call(batch=0) == 1                     # bad shape
+    assert call(block=0) == 4
+    assert call(head_dim=96, tensor_dim=64) == 1  # head_dim > tensor_dim
+    assert call(ws_bytes=100) == 4                # workspace too small
+    assert b"workspace" in lib.svd_last_error()
+    assert call(tensor_dim=96, head_dim=96) == 6  # tensor width 64 or 128 only
