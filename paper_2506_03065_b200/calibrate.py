@@ -65,13 +65,14 @@ def block_key_mass(q, k, grid: BlockGrid):
     nb = grid.n_blocks
     lib = nat.lib()
     ws_bytes = int(lib.svd_key_mass_workspace(B, H, N))
-    ws = _workspace(dev, ws_bytes)
+    stream = torch.cuda.current_stream(dev)
+    ws = _workspace(dev, stream, ws_bytes)
     mass = torch.empty(B, H, nb, dtype=torch.float64, device=dev)
     nat.check(lib.svd_block_key_mass(
         nat.c_void_p(qt.data_ptr()), nat.c_void_p(kt.data_ptr()), nat.i64x4(qt.stride()),
         nat.i64x4(kt.stride()), B, H, N, d, D, int(grid.layout.block_size), 0,
         nat.c_void_p(ws.data_ptr()), ws_bytes, nat.c_void_p(mass.data_ptr()),
-        nat.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+        nat.c_void_p(stream.cuda_stream)))
     if was_numpy:
         return mass.cpu().numpy()
     return mass
@@ -80,11 +81,12 @@ def block_key_mass(q, k, grid: BlockGrid):
 _WORKSPACES: dict = {}
 
 
-def _workspace(dev, nbytes: int):
-    """A per-device scratch buffer of at least nbytes (grown, never shrunk)."""
+def _workspace(dev, stream, nbytes: int):
+    """A scratch buffer of at least nbytes per (device, stream): calls on one
+    stream are ordered, so they can share it (grown, never shrunk)."""
     import torch
 
-    key = dev.index
+    key = (dev.index, stream.cuda_stream)
     buf = _WORKSPACES.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = _WORKSPACES[key] = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
