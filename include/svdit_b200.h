@@ -144,6 +144,11 @@ int svd_plan_group_mask(const svd_plan* plan, int32_t g, uint8_t* active);
  * (patterns.py:363-366 active_key_blocks).  row_ptr: nb+1; col_idx: nnz. */
 int svd_plan_group_nnz(const svd_plan* plan, int32_t g, int64_t* nnz);
 int svd_plan_group_csr(const svd_plan* plan, int32_t g, int64_t* row_ptr, int64_t* col_idx);
+/* The plan restricted to the listed heads, in that order (head i of the
+ * subset = plan head heads[i]): the parent's groups, masks, schedules and KV
+ * lists are copied, not rebuilt (the host-buffer pipeline launches head
+ * chunks this way).  Not for shard plans. */
+int svd_plan_subset(const svd_plan* plan, const int32_t* heads, int32_t n_heads, svd_plan** out);
 /* Restrict the plan's work items to one rank's share (LPT by tile cost) for
  * head/q-range sharding over world ranks.  The shard writes its rows into
  * a packed [rows, d] buffer; svd_plan_shard_rows() reports the row count and

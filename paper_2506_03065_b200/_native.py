@@ -97,6 +97,7 @@ SIGNATURES = {
     "svd_plan_group_nnz": (c_int, [c_void_p, c_int32, POINTER(c_int64)]),
     "svd_plan_group_csr": (c_int, [c_void_p, c_int32, c_void_p, c_void_p]),
     "svd_plan_schedule": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "svd_plan_subset": (c_int, [c_void_p, c_void_p, c_int32, POINTER(c_void_p)]),
     "svd_plan_shard": (c_int, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),
     "svd_plan_shard_sm": (c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, POINTER(c_void_p)]),
     "svd_plan_shard_rows": (c_int, [c_void_p, POINTER(c_int64), c_void_p, c_void_p]),

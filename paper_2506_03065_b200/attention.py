@@ -45,7 +45,6 @@ class LayerPlan:
         self.n_heads = n_heads
         self.sharded = sharded
         self._dev_rows = None
-        self._sub = None
         self._finalizer = weakref.finalize(self, nat.lib().svd_plan_destroy, nat.c_void_p(handle))
 
     # -- construction
@@ -58,10 +57,7 @@ class LayerPlan:
         specs = (nat.SvdSpec * n)(*[nat.make_spec(s, keep) for s in assignment])
         out = nat.c_void_p()
         nat.check(nat.lib().svd_plan_create(nat.make_layout(layout), specs, n, nat.ctypes.byref(out)))
-        plan = cls(out.value, layout, n)
-        asg = list(assignment)
-        plan._sub = lambda heads: cls.from_specs([asg[h] for h in heads], layout)
-        return plan
+        return cls(out.value, layout, n)
 
     @classmethod
     def from_masks(cls, layout: TokenLayout, group_masks, head_group) -> "LayerPlan":
@@ -80,10 +76,7 @@ class LayerPlan:
         nat.check(nat.lib().svd_plan_create_from_masks(
             nat.make_layout(layout), ng, nat.ptr(skip), nat.ptr(masks), nat.ptr(hg), int(hg.size),
             nat.ctypes.byref(out)))
-        plan = cls(out.value, layout, int(hg.size))
-        gm = list(group_masks)
-        plan._sub = lambda heads: cls.from_masks(layout, gm, hg[list(heads)])
-        return plan
+        return cls(out.value, layout, int(hg.size))
 
     def head_subplan(self, h0: int, h1: int) -> "LayerPlan":
         """The plan restricted to heads [h0, h1) (cached): lets host-resident
@@ -95,9 +88,12 @@ class LayerPlan:
         cache = self.__dict__.setdefault("_subplans", {})
         heads = tuple(int(h) for h in heads)
         if heads not in cache:
-            if self._sub is None:
-                raise ConfigError("this plan cannot be split by heads")
-            cache[heads] = self._sub(heads)
+            if self.sharded:
+                raise ConfigError("a shard plan cannot be split by heads")
+            arr = np.ascontiguousarray(np.asarray(heads, dtype=np.int32))
+            out = nat.c_void_p()
+            nat.check(nat.lib().svd_plan_subset(self._handle, nat.ptr(arr), int(arr.size), nat.ctypes.byref(out)))
+            cache[heads] = LayerPlan(out.value, self.layout, len(heads))
         return cache[heads]
 
     # -- queries

@@ -140,17 +140,28 @@ static int build_mask(const NormSpec& spec, const Grid& g, const svd_layout* L, 
     return SVD_OK;
   }
   if (spec.mode == SVD_DIAGONAL) {
+    // |i - j| <= hw: a band
     const int64_t hw = spec.halfwidth;
-    for (int64_t i = 0; i < nb; ++i)
-      for (int64_t j = 0; j < nb; ++j) active[i * nb + j] = std::llabs(i - j) <= hw;
+    std::memset(active, 0, size_t(nb * nb));
+    for (int64_t i = 0; i < nb; ++i) {
+      const int64_t j0 = std::max<int64_t>(0, i - hw), j1 = std::min<int64_t>(nb - 1, i + hw);
+      if (j0 <= j1) std::memset(active + i * nb + j0, 1, size_t(j1 - j0 + 1));
+    }
   } else if (spec.mode == SVD_MULTI_DIAGONAL) {
+    // f = |i - j| mod P; active when f <= hw or P - f <= hw: the pattern of
+    // row i is the distance pattern of one period, repeated
     const int64_t period = spec.period > 0 ? spec.period : frame_period(L);
     const int64_t hw = spec.md_halfwidth;
-    for (int64_t i = 0; i < nb; ++i)
-      for (int64_t j = 0; j < nb; ++j) {
-        const int64_t folded = std::llabs(i - j) % period;
-        active[i * nb + j] = (folded <= hw) || (period - folded <= hw);
-      }
+    std::vector<uint8_t> by_dist(static_cast<size_t>(nb));
+    for (int64_t dist = 0; dist < nb; ++dist) {
+      const int64_t folded = dist % period;
+      by_dist[dist] = (folded <= hw) || (period - folded <= hw);
+    }
+    for (int64_t i = 0; i < nb; ++i) {
+      uint8_t* row = active + i * nb;
+      std::reverse_copy(by_dist.begin() + 1, by_dist.begin() + i + 1, row);  // row[j] = by_dist[i - j]
+      std::memcpy(row + i, by_dist.data(), size_t(nb - i));
+    }
   } else {  // VERTICAL_STRIPE
     if (spec.stripes_none)
       return fail(SVD_ERR_CONFIG,
@@ -191,6 +202,31 @@ static void segment_keysets(const Group& grp, const Grid& g, int64_t nseg,
   const int64_t nb = g.nb, bs = g.bs, n = g.n;
   const int64_t words = (nseg + 63) / 64;
   keyset->assign(nseg, std::vector<uint64_t>(words, 0));
+  if (bs % kSeg == 0) {
+    // block-aligned segments (block_size 64, 128, ...): segment s lies in block
+    // s / r and key segment ks in block ks / r — bits straight from the mask row
+    const int64_t r = bs / kSeg;
+    std::vector<uint64_t> bits(words);
+    for (int64_t b = 0; b < nb; ++b) {
+      const uint8_t* row = grp.active.data() + b * nb;
+      std::fill(bits.begin(), bits.end(), 0);
+      if (r == 1) {
+        int64_t j = 0;
+        for (; j + 8 <= nb; j += 8) {  // eight 0/1 bytes -> eight bits
+          uint64_t x;
+          std::memcpy(&x, row + j, 8);
+          bits[j >> 6] |= ((x * 0x0102040810204080ull) >> 56) << (j & 63);
+        }
+        for (; j < nb; ++j) bits[j >> 6] |= uint64_t(row[j] != 0) << (j & 63);
+      } else {
+        for (int64_t j = 0; j < nb; ++j)
+          if (row[j])
+            for (int64_t ks = j * r; ks < std::min((j + 1) * r, nseg); ++ks) bits[ks >> 6] |= 1ull << (ks & 63);
+      }
+      for (int64_t s = b * r; s < std::min((b + 1) * r, nseg); ++s) (*keyset)[s] = bits;
+    }
+    return;
+  }
   std::vector<uint8_t> row(nb);
   std::vector<int64_t> prefix(nb + 1);
   for (int64_t s = 0; s < nseg; ++s) {
@@ -274,14 +310,16 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
   const bool tail_partial = (P->grid.n % kSeg) != 0;
   const int64_t words = (nseg + 63) / 64;
   std::vector<uint64_t> uni(words);
+  std::vector<int32_t> keys;
+  keys.reserve(size_t(nseg));
   for (auto& q : grp.qgroups) {
     std::fill(uni.begin(), uni.end(), 0);
     for (int k = 0; k < kSlotsPerItem; ++k)
       if (q[k] >= 0)
         for (int64_t w = 0; w < words; ++w) uni[w] |= keyset[q[k]][w];
-    std::vector<int32_t> keys;
-    for (int64_t ks = 0; ks < nseg; ++ks)
-      if (bit_of(uni, ks)) keys.push_back(int32_t(ks));
+    keys.clear();
+    for (int64_t w = 0; w < words; ++w)
+      for (uint64_t m = uni[w]; m; m &= m - 1) keys.push_back(int32_t(w * 64 + __builtin_ctzll(m)));
     grp.qgroup_kv_begin.push_back(int32_t(P->kv.size()));
     for (size_t i = 0; i < keys.size(); i += 2) {
       KvEntry e{};
@@ -311,17 +349,21 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
 static double group_active_pairs(const Group& grp, const Grid& g) {
   if (grp.skip) return 0.0;
   const int64_t nb = g.nb;
+  // every block holds bs tokens except the last: cols = bs * count - short(last)
+  const int64_t last_short = g.bs - (g.bounds[nb] - g.bounds[nb - 1]);
   double total = 0.0;
   for (int64_t i = 0; i < nb; ++i) {
-    const double rows = double(g.bounds[i + 1] - g.bounds[i]);
-    double cols = 0.0;
-    for (int64_t j = 0; j < nb; ++j)
-      if (grp.active[i * nb + j]) cols += double(g.bounds[j + 1] - g.bounds[j]);
-    total += rows * cols;
+    const uint8_t* row = grp.active.data() + i * nb;
+    int64_t count = 0;
+    for (int64_t j = 0; j < nb; ++j) count += row[j] != 0;
+    const int64_t cols = g.bs * count - (row[nb - 1] ? last_short : 0);
+    total += double(g.bounds[i + 1] - g.bounds[i]) * double(cols);
   }
   return total;
 }
 
+
+static void build_items(svd_plan* P);
 
 static void finalize_plan(svd_plan* P) {
   // query segments per CTA: two 128-row tiles ping-ponging in the kernel
@@ -346,11 +388,17 @@ static void finalize_plan(svd_plan* P) {
           if (grp.active[i * nb + j]) base[i * wpr + (j >> 5)] |= 1u << (j & 31);
     }
   }
+  for (auto& grp : P->groups) grp.pairs = group_active_pairs(grp, P->grid);
+  build_items(P);
+}
+
+// Work items of every (group, head, query-segment cluster), heaviest first.
+static void build_items(svd_plan* P) {
   P->items.clear();
   P->active_pairs = 0.0;
   for (size_t gi = 0; gi < P->groups.size(); ++gi) {
     const Group& grp = P->groups[gi];
-    P->active_pairs += double(grp.heads.size()) * group_active_pairs(grp, P->grid);
+    P->active_pairs += double(grp.heads.size()) * grp.pairs;
     for (int32_t h : grp.heads) {
       for (size_t qi = 0; qi < grp.qgroups.size(); ++qi) {
         WorkItem it{};
@@ -638,6 +686,66 @@ int svd_plan_schedule(const svd_plan* P, int32_t* items, int32_t* kv) {
   if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
   if (items) std::memcpy(items, P->items.data(), P->items.size() * sizeof(WorkItem));
   if (kv) std::memcpy(kv, P->kv.data(), P->kv.size() * sizeof(KvEntry));
+  return SVD_OK;
+}
+
+int svd_plan_subset(const svd_plan* P, const int32_t* heads, int32_t n_heads, svd_plan** out) {
+  if (!P || !heads || !out) return fail(SVD_ERR_CONFIG, "NULL argument");
+  *out = nullptr;
+  if (P->sharded) return fail(SVD_ERR_CONFIG, "a shard plan cannot be subset by heads");
+  if (n_heads < 1) return fail(SVD_ERR_CONFIG, "need at least one head");
+  std::vector<uint8_t> seen(P->n_heads, 0);
+  for (int32_t i = 0; i < n_heads; ++i) {
+    if (heads[i] < 0 || heads[i] >= P->n_heads) return fail(SVD_ERR_CONFIG, "head out of range");
+    if (seen[heads[i]]++) return fail(SVD_ERR_CONFIG, "duplicate head");
+  }
+  auto* S = new svd_plan();
+  S->layout = P->layout;
+  S->grid = P->grid;
+  S->nseg = P->nseg;
+  S->fine = P->fine;
+  S->cluster = P->cluster;
+  S->n_heads = n_heads;
+  S->head_group.resize(n_heads);
+  // the parent's groups in first-occurrence order of the listed heads, each
+  // with its mask, schedule and KV list copied (nothing is rebuilt)
+  std::vector<int32_t> remap(P->groups.size(), -1);
+  const int64_t wpr = (P->grid.nb + 31) / 32;
+  for (int32_t i = 0; i < n_heads; ++i) {
+    const int32_t pg = P->head_group[heads[i]];
+    if (remap[pg] < 0) {
+      remap[pg] = int32_t(S->groups.size());
+      const Group& src = P->groups[pg];
+      Group g;
+      g.spec = src.spec;
+      g.skip = src.skip;
+      g.active = src.active;
+      g.qgroups = src.qgroups;
+      g.qgroup_kv_count = src.qgroup_kv_count;
+      g.pairs = src.pairs;
+      int64_t kv0 = 0, kv1 = 0;
+      if (!src.qgroups.empty()) {
+        kv0 = src.qgroup_kv_begin.front();
+        kv1 = int64_t(src.qgroup_kv_begin.back()) + src.qgroup_kv_count.back();
+      }
+      const int64_t base = int64_t(S->kv.size());
+      for (size_t q = 0; q < src.qgroups.size(); ++q)  // SKIP clusters keep begin 0, count 0
+        g.qgroup_kv_begin.push_back(src.skip ? 0 : int32_t(src.qgroup_kv_begin[q] - kv0 + base));
+      S->kv.insert(S->kv.end(), P->kv.begin() + kv0, P->kv.begin() + kv1);
+      if (P->fine && !src.skip) {
+        S->fine_bit_off.push_back(int64_t(S->fine_bits.size()));
+        const auto* b = P->fine_bits.data() + P->fine_bit_off[pg];
+        S->fine_bits.insert(S->fine_bits.end(), b, b + P->grid.nb * wpr);
+      } else {
+        S->fine_bit_off.push_back(-1);
+      }
+      S->groups.push_back(std::move(g));
+    }
+    S->head_group[i] = remap[pg];
+    S->groups[remap[pg]].heads.push_back(i);
+  }
+  build_items(S);
+  *out = S;
   return SVD_OK;
 }
 

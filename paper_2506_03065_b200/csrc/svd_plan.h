@@ -74,6 +74,7 @@ struct Group {
   // kernel schedule for this group (shared by all its heads)
   std::vector<std::array<int32_t, kSlotsPerItem>> qgroups;
   std::vector<int32_t> qgroup_kv_begin, qgroup_kv_count;
+  double pairs = 0.0;  // active (query token, key token) pairs of one head
 };
 
 struct DeviceTables {

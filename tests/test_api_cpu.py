@@ -250,3 +250,63 @@ def test_plugin_surface_matches_the_reference():
     for strat in ("per_step", "majority_over_steps"):
         np.testing.assert_array_equal(S.aggregate_config(ours, lay_ours, strat).modes,
                                       RS.aggregate_config(ref, lay_ref, strat).modes)
+
+
+def test_heads_subplan_copies_the_parent_schedule():
+    """svd_plan_subset: a head subset (any order) carries exactly the work
+    items and KV lists a fresh plan of those heads' specs builds; bad head
+    lists and shard plans are rejected."""
+    import numpy as np
+
+    layout = S.TokenLayout(40, 6, 300, 64)
+    asg = [S.full_spec(), S.diagonal_spec(1), S.skip_spec(), S.multi_diagonal_spec(),
+           S.vertical_stripe_spec(stripes=(3, 20)), S.diagonal_spec(1)]
+    plan = S.plan_for_assignment(asg, layout)
+    for heads in [(4, 1), (0,), (5, 2, 3), (1, 5)]:
+        sub = plan.heads_subplan(heads)
+        fresh = S.LayerPlan.from_specs([asg[h] for h in heads], layout)
+        (ia, ka), (ib, kb) = sub.schedule(), fresh.schedule()
+        assert np.array_equal(ia, ib) and np.array_equal(ka, kb)
+        assert sub.info.n_groups == fresh.info.n_groups
+        assert sub.active_flops(64) == fresh.active_flops(64)
+        for g in range(sub.info.n_groups):
+            assert sub.group_heads(g) == fresh.group_heads(g)
+    for bad in [(1, 1), (9,)]:
+        with pytest.raises(S.ConfigError):
+            plan.heads_subplan(bad)
+    with pytest.raises(S.ConfigError):
+        plan.shard(2, 0, n_sms=148).heads_subplan((0,))
+
+
+@pytest.mark.parametrize("block", [64, 128, 32, 48])
+def test_plan_schedule_matches_masks(block):
+    """Every work item's KV tiles cover exactly the segments its rows need
+    (active blocks of the group mask), for block sizes on and off the
+    64-token segment grain (the fast block-aligned keyset path and the general one)."""
+    import numpy as np
+
+    layout = S.TokenLayout(70, 5, 333, block)
+    asg = [S.diagonal_spec(1), S.multi_diagonal_spec(period=3), S.vertical_stripe_spec(stripes=(2, 7))]
+    plan = S.plan_for_assignment(asg, layout)
+    grid = S.block_grid(layout)
+    n, nseg = layout.total_tokens, -(-layout.total_tokens // 64)
+    items, kv = plan.schedule()
+    for g in range(plan.info.n_groups):
+        heads, skip = plan.group_heads(g)
+        m = plan.group_mask(g)
+        blk = np.minimum(np.arange(nseg * 64) // block, grid.n_blocks - 1)
+        need = {}
+        for s in range(nseg):
+            rows = np.unique(blk[s * 64:min((s + 1) * 64, n)])
+            cols = np.flatnonzero(m[rows].any(axis=0))
+            segs = set()
+            for c in cols:
+                c0, c1 = grid.bounds[c], grid.bounds[c + 1]
+                segs.update(range(c0 // 64, (c1 - 1) // 64 + 1))
+            need[s] = segs
+        for it in items[items[:, 0] == heads[0]]:
+            got = set()
+            for e in kv[it[2]:it[2] + it[3]]:
+                got.update(x for x in e[:2] if x >= 0)
+            want = set().union(*(need[s] for s in it[4:8] if s >= 0))
+            assert got == want
