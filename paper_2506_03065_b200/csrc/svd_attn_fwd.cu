@@ -158,7 +158,23 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* tmap, uint32_t dst,
 
 // Mask one 128-key tile of S for this thread's row.  Segment-grain tiles
 // (block_size % 64 == 0) need only the tile's activity bits and the sequence
-// end; FINE (block_size % 64 != 0) looks up every element's (qb, kb) bit.
+// end; FINE (block_size % 64 != 0) builds each key segment's 64-bit key mask
+// from the few blocks it overlaps (one bit lookup per block), then selects.
+__device__ __forceinline__ uint64_t fine_segment_mask(int seg, int lim, const FwdParams& p,
+                                                      const uint32_t* bits_row) {
+  if (lim <= 0) return 0ull;
+  const int c0 = seg * kSeg;
+  const int kb_first = c0 / p.block_size, kb_last = (c0 + lim - 1) / p.block_size;
+  uint64_t m = 0ull;
+  for (int kb = kb_first; kb <= kb_last; ++kb) {
+    if (!((__ldg(bits_row + (kb >> 5)) >> (kb & 31)) & 1u)) continue;
+    const int lo = max(kb * p.block_size - c0, 0), hi = min((kb + 1) * p.block_size - c0, lim);
+    const uint64_t upto_hi = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+    m |= upto_hi & ~((1ull << lo) - 1ull);
+  }
+  return m;
+}
+
 template <bool FINE>
 __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, int qslot,
                                            const FwdParams& p, const uint32_t* bits_row) {
@@ -167,18 +183,12 @@ __device__ __forceinline__ void apply_mask(float (&s)[128], const KvEntry& e, in
   const int lim0 = on0 ? min(kSeg, p.n_tokens - e.kseg0 * kSeg) : 0;
   const int lim1 = (on1 && e.kseg1 >= 0) ? min(kSeg, p.n_tokens - e.kseg1 * kSeg) : 0;
   if constexpr (FINE) {
+    const uint64_t m0 = fine_segment_mask(e.kseg0, lim0, p, bits_row);
+    const uint64_t m1 = fine_segment_mask(e.kseg1, lim1, p, bits_row);
+    const uint32_t w[4] = {uint32_t(m0), uint32_t(m0 >> 32), uint32_t(m1), uint32_t(m1 >> 32)};
 #pragma unroll
-    for (int i = 0; i < 128; ++i) {
-      const int slot = i >> 6;
-      const int lim = slot ? lim1 : lim0;
-      const int c = (slot ? e.kseg1 : e.kseg0) * kSeg + (i & 63);
-      bool ok = (i & 63) < lim;
-      if (ok) {
-        const int kb = c / p.block_size;
-        ok = (__ldg(bits_row + (kb >> 5)) >> (kb & 31)) & 1u;
-      }
-      if (!ok) s[i] = -INFINITY;
-    }
+    for (int i = 0; i < 128; ++i)
+      if (!((w[i >> 5] >> (i & 31)) & 1u)) s[i] = -INFINITY;
   } else {
 #pragma unroll
     for (int i = 0; i < 64; ++i) {

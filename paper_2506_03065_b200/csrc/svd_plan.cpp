@@ -197,8 +197,12 @@ static int build_mask(const NormSpec& spec, const Grid& g, const svd_layout* L, 
 // ---------------------------------------------------------------- schedule
 // Segment-level key sets of one group: keyset[s] bit ks is set when any
 // active (qb, kb) pair touches query segment s and key segment ks.
+// fullset (FINE grids only, block_size % 64 != 0): bit ks set when EVERY
+// (qb, kb) pair overlapping segments (s, ks) is active — such tiles need no
+// per-element mask in the kernel.
 static void segment_keysets(const Group& grp, const Grid& g, int64_t nseg,
-                            std::vector<std::vector<uint64_t>>* keyset) {
+                            std::vector<std::vector<uint64_t>>* keyset,
+                            std::vector<std::vector<uint64_t>>* fullset) {
   const int64_t nb = g.nb, bs = g.bs, n = g.n;
   const int64_t words = (nseg + 63) / 64;
   keyset->assign(nseg, std::vector<uint64_t>(words, 0));
@@ -227,21 +231,31 @@ static void segment_keysets(const Group& grp, const Grid& g, int64_t nseg,
     }
     return;
   }
-  std::vector<uint8_t> row(nb);
-  std::vector<int64_t> prefix(nb + 1);
+  fullset->assign(nseg, std::vector<uint64_t>(words, 0));
+  std::vector<uint8_t> row(nb), row_all(nb);
+  std::vector<int64_t> prefix(nb + 1), prefix_all(nb + 1);
   for (int64_t s = 0; s < nseg; ++s) {
     const int64_t t0 = s * kSeg, t1 = std::min(t0 + kSeg, n);
     const int64_t b0 = t0 / bs, b1 = (t1 - 1) / bs;
     std::fill(row.begin(), row.end(), 0);
+    std::fill(row_all.begin(), row_all.end(), 1);
     for (int64_t b = b0; b <= b1; ++b)
-      for (int64_t j = 0; j < nb; ++j) row[j] |= grp.active[b * nb + j];
-    prefix[0] = 0;
-    for (int64_t j = 0; j < nb; ++j) prefix[j + 1] = prefix[j] + row[j];
+      for (int64_t j = 0; j < nb; ++j) {
+        row[j] |= grp.active[b * nb + j];
+        row_all[j] &= grp.active[b * nb + j] != 0;
+      }
+    prefix[0] = prefix_all[0] = 0;
+    for (int64_t j = 0; j < nb; ++j) {
+      prefix[j + 1] = prefix[j] + row[j];
+      prefix_all[j + 1] = prefix_all[j] + row_all[j];
+    }
     auto& ks_bits = (*keyset)[s];
+    auto& full_bits = (*fullset)[s];
     for (int64_t ks = 0; ks < nseg; ++ks) {
       const int64_t c0 = ks * kSeg, c1 = std::min(c0 + kSeg, n);
       const int64_t k0 = c0 / bs, k1 = (c1 - 1) / bs;
       if (prefix[k1 + 1] - prefix[k0] > 0) ks_bits[ks >> 6] |= 1ull << (ks & 63);
+      if (prefix_all[k1 + 1] - prefix_all[k0] == k1 - k0 + 1) full_bits[ks >> 6] |= 1ull << (ks & 63);
     }
   }
 }
@@ -304,8 +318,10 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
     }
     return;
   }
-  std::vector<std::vector<uint64_t>> keyset;
-  segment_keysets(grp, P->grid, nseg, &keyset);
+  std::vector<std::vector<uint64_t>> keyset, fullset;
+  segment_keysets(grp, P->grid, nseg, &keyset, &fullset);
+  // segment-grain grids: an active segment pair is one active block pair
+  const auto& full = P->fine ? fullset : keyset;
   grp.qgroups = cluster_segments(keyset, nseg, P->cluster);
   const bool tail_partial = (P->grid.n % kSeg) != 0;
   const int64_t words = (nseg + 63) / 64;
@@ -326,7 +342,7 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
       e.kseg0 = keys[i];
       e.kseg1 = i + 1 < keys.size() ? keys[i + 1] : -1;
       uint32_t bits = 0;
-      bool all = e.kseg1 >= 0 && !P->fine;
+      bool all = e.kseg1 >= 0;
       for (int slot = 0; slot < kSlotsPerItem; ++slot) {
         for (int kslot = 0; kslot < 2; ++kslot) {
           const int32_t ks = kslot == 0 ? e.kseg0 : e.kseg1;
@@ -334,7 +350,8 @@ static void build_group_schedule(svd_plan* P, Group& grp) {
           if (q[slot] < 0) on = true;  // empty q slot: never stored
           else on = ks >= 0 && bit_of(keyset[q[slot]], ks);
           if (on) bits |= 1u << (2 * slot + kslot);
-          else all = false;
+          // FINE: "all" also needs every block pair under the segment pair active
+          if (!on || (q[slot] >= 0 && !bit_of(full[q[slot]], ks))) all = false;
         }
       }
       const bool tail = tail_partial && (e.kseg0 == nseg - 1 || e.kseg1 == nseg - 1);

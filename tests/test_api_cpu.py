@@ -286,14 +286,16 @@ def test_plan_schedule_matches_masks(block):
     import numpy as np
 
     layout = S.TokenLayout(70, 5, 333, block)
-    asg = [S.diagonal_spec(1), S.multi_diagonal_spec(period=3), S.vertical_stripe_spec(stripes=(2, 7))]
+    asg = [S.diagonal_spec(1), S.multi_diagonal_spec(period=3), S.vertical_stripe_spec(stripes=(2, 7)),
+           S.full_spec()]
     plan = S.plan_for_assignment(asg, layout)
     grid = S.block_grid(layout)
     n, nseg = layout.total_tokens, -(-layout.total_tokens // 64)
     items, kv = plan.schedule()
+    n_all = 0
     for g in range(plan.info.n_groups):
         heads, skip = plan.group_heads(g)
-        m = plan.group_mask(g)
+        m = plan.group_mask(g) if int(asg[heads[0]].mode) != 0 else np.ones((grid.n_blocks,) * 2, bool)
         blk = np.minimum(np.arange(nseg * 64) // block, grid.n_blocks - 1)
         need = {}
         for s in range(nseg):
@@ -308,5 +310,14 @@ def test_plan_schedule_matches_masks(block):
             got = set()
             for e in kv[it[2]:it[2] + it[3]]:
                 got.update(x for x in e[:2] if x >= 0)
+                if e[2] & (1 << 8):  # kFlagAll: the kernel applies no mask to this tile
+                    n_all += 1
+                    assert e[1] >= 0
+                    for qs in (x for x in it[4:8] if x >= 0):
+                        qb = np.unique(blk[qs * 64:min((qs + 1) * 64, n)])
+                        kb = np.unique(blk[e[0] * 64:min(e[0] * 64 + 64, n)].tolist()
+                                       + blk[e[1] * 64:min(e[1] * 64 + 64, n)].tolist())
+                        assert m[np.ix_(qb, kb)].all()
             want = set().union(*(need[s] for s in it[4:8] if s >= 0))
             assert got == want
+    assert n_all > 0  # the FULL head's interior tiles at least
