@@ -418,6 +418,23 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt[0])
 
+    # the reference's own call with its own types: float32 NumPy in, float32
+    # NumPy out (attention.py:186-212), wall clock per call (1 GPU)
+    numpy_e2e = None
+    if world == 1:
+        nq, nk, nv = (t.float().numpy() for t in (hq, hk, hv))
+        S.fused_layer_attention(nq, nk, nv, groups)
+        walls = []
+        for _ in range(3):
+            w0 = time.perf_counter()
+            S.fused_layer_attention(nq, nk, nv, groups)
+            walls.append(round((time.perf_counter() - w0) * 1e3, 2))
+        numpy_e2e = {"ms_per_layer": min(walls), "wall_ms_steps": walls,
+                     "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1],
+                     "path": ("fused_layer_attention(float32 NumPy q/k/v) -> float32 NumPy: converted to "
+                              "bf16 on the host cores chunk by chunk into pinned staging, same pipeline")}
+        del nq, nk, nv
+
     # dense sm_100a baseline on the same GPU: every head FULL through the same kernel
     dense_ms = None
     if not args.no_dense and world == 1:
@@ -500,6 +517,7 @@ def run_ours(args):
                      "chunked by a flow-shop model, H2D / kernel / D2H streams overlapped; SKIP heads "
                      "never cross PCIe (zeros written on the host)"),
         },
+        "e2e_reference_types": numpy_e2e,
         "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),
         "clocks": clock,
     }

@@ -478,6 +478,19 @@ class _Staging:
         self.lock = threading.Lock()
         self._maps = {}
         self._dev = dev
+        self._host = {}
+
+    def host_buffers(self, kind: str, count: int, B: int, N: int, d: int):
+        """Resident pinned bf16 host staging [B, H, N, d] (slot-indexed like
+        the device staging) for inputs / results that are not pinned bf16."""
+        import torch
+
+        bufs = self._host.get(kind)
+        if bufs is None:
+            H = self.qkv[0].shape[1]
+            bufs = self._host[kind] = [torch.empty((B, H, N, d), dtype=torch.bfloat16, pin_memory=True)
+                                       for _ in range(count)]
+        return bufs
 
     def head_map(self, order, s0: int, s1: int):
         """Device int32 tensor of the output heads of staging slots [s0, s1)."""
@@ -511,12 +524,18 @@ def _check_out(out, shape, device_type: str):
         raise ShapeError("out must have a unit-stride last dimension")
 
 
-def _run_host(plan: LayerPlan, q, k, v, out=None):
+def _run_host(plan: LayerPlan, q, k, v, out=None, numpy_out: bool = False):
     """Host (CPU torch) tensors: pipeline head chunks through copy-in,
     compute and copy-out streams so the PCIe/C2C transfers overlap the kernel
     (the end-to-end path of the operator with host buffers).  Returns a CPU
     bf16 tensor (pinned), or writes `out` (a caller-owned, ideally pinned, CPU
-    bf16 tensor: no per-call host allocation)."""
+    bf16 tensor: no per-call host allocation); numpy_out: a float32 NumPy
+    result checked for finiteness (the reference's own types).
+
+    Inputs that are not pinned bf16 (e.g. the reference's float32 NumPy
+    arrays) are converted chunk by chunk on the host's cores into resident
+    pinned bf16 staging, so the conversion of chunk c+1 overlaps the copies
+    and the kernel of chunk c, and only bf16 crosses PCIe."""
     import torch
 
     B, H, N, d = q.shape
@@ -524,7 +543,10 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
     D = _tensor_dim(d)
     order, bounds = _host_schedule(plan, B, N, d)
     chunks = len(bounds) - 1
-    if out is None:
+    if numpy_out:
+        res = np.empty((B, H, N, d), dtype=np.float32)
+        out_host = torch.from_numpy(res)
+    elif out is None:
         out_host = torch.empty((B, H, N, d), dtype=torch.bfloat16, pin_memory=True)
     else:
         _check_out(out, (B, H, N, d), "cpu")
@@ -532,62 +554,87 @@ def _run_host(plan: LayerPlan, q, k, v, out=None):
     skip = plan.skip_heads()
     if chunks == 0:  # every head SKIP
         out_host.zero_()
-        return out_host
+        return res if numpy_out else out_host
     # staging slot s holds head order[s]; chunks are contiguous slot ranges
     st = _host_staging(plan, dev, B, N, d, D)
+    direct_in = all(x.dtype == torch.bfloat16 and x.is_pinned() for x in (q, k, v))
+    direct_out = not numpy_out and out_host.is_pinned()
     with st.lock:
+        host_in = None if direct_in else st.host_buffers("in", 3, B, N, d)
+        host_out = None if direct_out else st.host_buffers("out", 1, B, N, d)[0]
         compute = torch.cuda.current_stream(dev)
         s_in, s_out = st.s_in, st.s_out
-        loaded = []
-        with torch.cuda.stream(s_in):
-            for c in range(chunks):
-                for slot in range(bounds[c], bounds[c + 1]):
-                    h = order[slot]
-                    for x, buf in zip((q, k, v), st.qkv):
-                        xc = x[:, h]
-                        if xc.dtype != torch.bfloat16:
-                            xc = xc.to(torch.bfloat16)
-                        if not xc.is_pinned():
-                            xc = xc.contiguous().pin_memory()
-                        buf[:, slot, :, :d].copy_(xc, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(s_in)
-                loaded.append(ev)
         # zero-copy result: the kernel stores rows straight into the pinned
         # host O through a per-chunk head map (no copy-out stage to drain)
-        zero_copy = HOST_ZERO_COPY and D == d and out_host.is_pinned() and out_host.is_contiguous()
-        computed = []
+        zero_copy = (HOST_ZERO_COPY and D == d and direct_out and out_host.is_contiguous())
         streams = (compute, st.s_comp) if HOST_OVERLAP else (compute,)
         st.s_comp.wait_stream(compute)  # the caller's prior work on its stream
+        finite = []
+        copied = []   # per chunk: D2H done event
+        drained = 0   # chunks whose results are in out_host
+
+        def drain(upto: int, block: bool) -> int:
+            # host-side finish of chunks [drained, upto): widen to out_host
+            n_done = drained
+            while n_done < upto:
+                if not block and not copied[n_done].query():
+                    break
+                copied[n_done].synchronize()
+                for slot in range(bounds[n_done], bounds[n_done + 1]):
+                    out_host[:, order[slot]].copy_(host_out[:, slot])
+                n_done += 1
+            return n_done
+
         for c in range(chunks):
             s0, s1 = bounds[c], bounds[c + 1]
+            with torch.cuda.stream(s_in):
+                for slot in range(s0, s1):
+                    h = order[slot]
+                    for i, (x, buf) in enumerate(zip((q, k, v), st.qkv)):
+                        xc = x[:, h]
+                        if not direct_in:  # widen / narrow on the host cores into pinned bf16
+                            host_in[i][:, slot].copy_(xc)
+                            xc = host_in[i][:, slot]
+                        buf[:, slot, :, :d].copy_(xc, non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(s_in)
             cs = streams[c % len(streams)]
-            cs.wait_event(loaded[c])
+            cs.wait_event(loaded)
             qc, kc, vc = (buf[:, s0:s1] for buf in st.qkv)
             sub = plan.heads_subplan(tuple(order[s0:s1]))
             if zero_copy:
                 sub.forward(qc, kc, vc, out_host, head_dim=d, stream=cs,
                             o_head_map=st.head_map(order, s0, s1))
-            else:
-                sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=cs)
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            computed.append(ev)
+                continue
+            sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=cs)
+            computed = torch.cuda.Event()
+            computed.record(cs)
+            if numpy_out:  # attention.py:98 require_finite, reduced on the device
+                with torch.cuda.stream(cs):
+                    finite.append(torch.isfinite(st.o[:, s0:s1, :, :d]).all())
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(computed)
+                for slot in range(s0, s1):
+                    dst = out_host[:, order[slot]] if direct_out else host_out[:, slot]
+                    dst.copy_(st.o[:, slot, :, :d], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_out)
+                copied.append(ev)
+            if not direct_out:
+                drained = drain(c, block=False)
         if len(streams) > 1:
             compute.wait_stream(st.s_comp)  # the caller's stream sees every chunk
-        with torch.cuda.stream(s_out):
-            if not zero_copy:
-                for c in range(chunks):
-                    s_out.wait_event(computed[c])
-                    for slot in range(bounds[c], bounds[c + 1]):
-                        out_host[:, order[slot]].copy_(st.o[:, slot, :, :d], non_blocking=True)
         for h in skip:  # SKIP heads (attention.py:51-54): zeros written on the host, under the GPU work
             out_host[:, h].zero_()
         if zero_copy:
             compute.synchronize()
-        else:
+        elif direct_out:
             s_out.synchronize()  # a host result must be readable on return
-    return out_host
+        else:
+            drain(chunks, block=True)
+        if numpy_out and not bool(torch.stack(finite).all()):
+            raise ShapeError("non-finite values in attention output")
+    return res if numpy_out else out_host
 
 
 def host_transfer_bytes(plan: LayerPlan, B: int, N: int, d: int) -> tuple[int, int]:
@@ -616,6 +663,13 @@ def _run(plan: LayerPlan, q, k, v, out=None):
         raise ConfigError(f"plan covers {plan.n_heads} heads, tensors have {H}")
     if out is not None and not _is_torch(q):
         raise ShapeError("out= is supported for torch tensors only")
+    if not _is_torch(q):
+        # the reference's own types (float32 NumPy in and out): the pipelined
+        # host path, converting on the host cores chunk by chunk
+        if not torch.cuda.is_available():
+            raise nat.NativeError("a CUDA device is required: the sm_100a kernel has no CPU path")
+        ts = [torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32))) for x in (q, k, v)]
+        return _run_host(plan, *ts, numpy_out=True)
     (qt, kt, vt), was_numpy, dev = _to_device((q, k, v))
     dt = qt.shape[-1]
     if out is not None:
