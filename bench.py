@@ -407,16 +407,24 @@ def run_ours(args):
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    # bytes copied per step: one GPU pipelines every non-SKIP head's Q/K/V in and
-    # O out; a shard rank copies the full Q/K/V in and the full O out
-    e2e_bytes = (S.host_transfer_bytes(plan, 1, n, d) if world == 1
-                 else (3 * H * n * d * 2, H * n * d * 2))
+    # bytes copied per step (whole job): one GPU pipelines every non-SKIP head's
+    # Q/K/V in and O out; a peer-memory shard rank copies its own head range in
+    # and out, an NCCL shard rank the full Q/K/V in and the full O out
+    if world == 1:
+        e2e_bytes = S.host_transfer_bytes(plan, 1, n, d)
+    elif mgpu == "p2p":
+        e2e_bytes = layer.e2e_bytes((1, H, n, d))
+    else:
+        e2e_bytes = (3 * H * n * d * 2, H * n * d * 2)
     if world > 1:
         import torch.distributed as dist
 
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt[0])
+        bt = torch.tensor(list(e2e_bytes), device=dev, dtype=torch.float64)
+        dist.all_reduce(bt, op=dist.ReduceOp.SUM)
+        e2e_bytes = (int(bt[0]), int(bt[1]))
 
     # the reference's own call with its own types: float32 NumPy in, float32
     # NumPy out (attention.py:186-212), wall clock per call (1 GPU)
@@ -515,7 +523,10 @@ def run_ours(args):
             "d2h_bytes_per_step": e2e_bytes[1],
             "path": ("fused_layer_attention(pinned host bf16 Q/K/V, out=pinned O): heads reordered and "
                      "chunked by a flow-shop model, H2D / kernel / D2H streams overlapped; SKIP heads "
-                     "never cross PCIe (zeros written on the host)"),
+                     "never cross PCIe (zeros written on the host)") if world == 1 else
+                    ("per rank: H2D of its own heads (equal-cost head partition, ~H/N heads per rank), "
+                     "shard kernel storing rows into every rank's O over peer memory, D2H of its heads"
+                     if mgpu == "p2p" else "per rank: full H2D, shard kernel, NCCL all-gather, full D2H"),
         },
         "e2e_reference_types": numpy_e2e,
         "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),

@@ -160,6 +160,14 @@ int svd_plan_shard(const svd_plan* plan, int32_t world, int32_t rank, svd_plan**
  * svd_plan_shard does with n_sms = 148), < 0 = never split. */
 int svd_plan_shard_sm(const svd_plan* plan, int32_t world, int32_t rank, int32_t n_sms,
                       int32_t max_item_tiles, svd_plan** shard);
+/* As svd_plan_shard_sm, choosing how items are dealt to ranks:
+ * SVD_PARTITION_ITEMS — LPT over all items (any rank may touch any head);
+ * SVD_PARTITION_HEADS — contiguous head ranges of equal cost (McNaughton's
+ * wrap-around: at most the two boundary heads of a rank are split by query
+ * range), so a rank reads only its own heads' Q/K/V. */
+enum { SVD_PARTITION_ITEMS = 0, SVD_PARTITION_HEADS = 1 };
+int svd_plan_shard_ex(const svd_plan* plan, int32_t world, int32_t rank, int32_t n_sms,
+                      int32_t max_item_tiles, int32_t partition, svd_plan** shard);
 int svd_plan_shard_rows(const svd_plan* shard, int64_t* n_rows, int32_t* row_head,
                         int32_t* row_token);
 

@@ -159,17 +159,28 @@ class LayerPlan:
         return 4.0 * head_dim * self.info.dense_pairs
 
     # -- multi-GPU
-    def shard(self, world: int, rank: int, n_sms: int | None = None, max_item_tiles: int = 0) -> "LayerPlan":
-        """This rank's share of the work items (LPT over ranks), with items
-        longer than max_item_tiles KV tiles split along the KV list and merged
-        in the kernel (0: an eighth of the shard's mean per-SM load on n_sms
-        SMs — the current device's count, 148 on B200; < 0: never split)."""
+    def shard(self, world: int, rank: int, n_sms: int | None = None, max_item_tiles: int = 0,
+              partition: str = "items") -> "LayerPlan":
+        """This rank's share of the work items, with items longer than
+        max_item_tiles KV tiles split along the KV list and merged in the
+        kernel (0: chosen by simulating every rank's SM packing on n_sms SMs —
+        the current device's count, 148 on B200; < 0: never split).
+        partition "items": LPT over all items; "heads": contiguous head ranges
+        of equal cost (a rank reads only its own heads' Q/K/V)."""
         if n_sms is None:
             n_sms = _device_sm_count()
+        part = {"items": 0, "heads": 1}.get(partition)
+        if part is None:
+            raise ConfigError(f"unknown partition {partition!r} (items | heads)")
         out = nat.c_void_p()
-        nat.check(nat.lib().svd_plan_shard_sm(self._handle, world, rank, int(n_sms), int(max_item_tiles),
+        nat.check(nat.lib().svd_plan_shard_ex(self._handle, world, rank, int(n_sms), int(max_item_tiles), part,
                                               nat.ctypes.byref(out)))
         return LayerPlan(out.value, self.layout, self.n_heads, sharded=True)
+
+    def shard_heads(self) -> tuple[int, ...]:
+        """Heads this shard's items touch (ascending)."""
+        items, _ = self.schedule()
+        return tuple(sorted({int(h) for h in items[:, 0]}))
 
     def shard_rows(self) -> tuple[np.ndarray, np.ndarray]:
         n = nat.c_int64(0)

@@ -766,11 +766,14 @@ int svd_plan_subset(const svd_plan* P, const int32_t* heads, int32_t n_heads, sv
   return SVD_OK;
 }
 
-int svd_plan_shard_sm(const svd_plan* P, int32_t world, int32_t rank, int32_t n_sms,
-                      int32_t max_item_tiles, svd_plan** shard) {
+int svd_plan_shard_ex(const svd_plan* P, int32_t world, int32_t rank, int32_t n_sms,
+                      int32_t max_item_tiles, int32_t partition, svd_plan** shard) {
   if (!P || !shard) return fail(SVD_ERR_CONFIG, "NULL argument");
+  if (P->sharded) return fail(SVD_ERR_CONFIG, "plan is already a shard");
   if (world < 1 || rank < 0 || rank >= world) return fail(SVD_ERR_CONFIG, "bad world/rank");
   if (n_sms < 1) return fail(SVD_ERR_CONFIG, "n_sms must be >= 1");
+  if (partition != SVD_PARTITION_ITEMS && partition != SVD_PARTITION_HEADS)
+    return fail(SVD_ERR_CONFIG, "unknown partition");
   auto* S = new svd_plan();
   S->layout = P->layout;
   S->grid = P->grid;
@@ -794,10 +797,53 @@ int svd_plan_shard_sm(const svd_plan* P, int32_t world, int32_t rank, int32_t n_
   };
   std::vector<double> load(world, 0.0);
   std::vector<int32_t> owner(P->items.size());
-  for (size_t i = 0; i < P->items.size(); ++i) {
-    const int32_t best = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
-    load[best] += item_cost(P->items[i]);
-    owner[i] = best;
+  if (partition == SVD_PARTITION_ITEMS) {
+    for (size_t i = 0; i < P->items.size(); ++i) {
+      const int32_t best = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
+      load[best] += item_cost(P->items[i]);
+      owner[i] = best;
+    }
+  } else {
+    // McNaughton's wrap-around over a head sequence: rank r takes the cost
+    // interval [r T, (r+1) T) of the head-ordered item sequence, so it holds
+    // whole heads except for at most the two boundary heads of its interval
+    // (split by query range) — its inputs are those heads only.  The sequence
+    // interleaves heavy and light heads so that every interval also covers
+    // about H / world heads (the rank's copy-in bytes): at each step the
+    // lightest remaining head if the running cost share is ahead of the
+    // running head share, else the heaviest.
+    const int32_t H = P->n_heads;
+    std::vector<std::vector<size_t>> by_head(static_cast<size_t>(H));
+    std::vector<double> hcost(static_cast<size_t>(H), 0.0);
+    double total = 0.0;
+    for (size_t i = 0; i < P->items.size(); ++i) {
+      by_head[size_t(P->items[i].head)].push_back(i);
+      hcost[size_t(P->items[i].head)] += item_cost(P->items[i]);
+      total += item_cost(P->items[i]);
+    }
+    std::vector<int32_t> desc(static_cast<size_t>(H));
+    for (int32_t h = 0; h < H; ++h) desc[size_t(h)] = h;
+    std::stable_sort(desc.begin(), desc.end(),
+                     [&](int32_t a, int32_t b) { return hcost[size_t(a)] > hcost[size_t(b)]; });
+    std::vector<int32_t> seq;
+    size_t lo = 0, hi = desc.size();
+    double seq_cost = 0.0;
+    while (lo < hi) {
+      const bool cost_ahead = seq_cost / total > double(seq.size()) / double(H);
+      const int32_t h = cost_ahead ? desc[--hi] : desc[lo++];
+      seq.push_back(h);
+      seq_cost += hcost[size_t(h)];
+    }
+    const double T = total / double(world);
+    double cum = 0.0;
+    for (int32_t h : seq)
+      for (size_t i : by_head[size_t(h)]) {
+        const double c = item_cost(P->items[i]);
+        const int32_t r = std::min<int32_t>(world - 1, int32_t((cum + 0.5 * c) / T));
+        owner[i] = r;
+        load[r] += c;
+        cum += c;
+      }
   }
   for (size_t i = 0; i < P->items.size(); ++i) {
     if (owner[i] != rank) continue;
@@ -865,6 +911,11 @@ int svd_plan_shard_sm(const svd_plan* P, int32_t world, int32_t rank, int32_t n_
   for (const auto& it : S->items) S->computed_tiles += 2 * int64_t(it.kv_count);
   *shard = S;
   return SVD_OK;
+}
+
+int svd_plan_shard_sm(const svd_plan* P, int32_t world, int32_t rank, int32_t n_sms,
+                      int32_t max_item_tiles, svd_plan** shard) {
+  return svd_plan_shard_ex(P, world, rank, n_sms, max_item_tiles, SVD_PARTITION_ITEMS, shard);
 }
 
 int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** shard) {

@@ -47,7 +47,7 @@ class PeerShardedLayer:
     """
 
     def __init__(self, plan: LayerPlan, world: int, rank: int, head_dim: int, device, shape,
-                 max_item_tiles: int | None = None):
+                 max_item_tiles: int | None = None, partition: str = "heads"):
         import torch
         import torch.distributed as dist
 
@@ -57,11 +57,15 @@ class PeerShardedLayer:
         self.head_dim = head_dim
         self.device = device
         # a shard view (split-KV balanced) for N > 1, the plain plan for one rank
-        # unless a split cap is forced (tests)
+        # unless a split cap is forced (tests).  "heads": contiguous head
+        # ranges of equal cost, so a rank's inputs are its own heads only
         if world > 1 or max_item_tiles is not None:
-            self.shard = plan.shard(world, rank, max_item_tiles=max_item_tiles or 0)
+            self.shard = plan.shard(world, rank, max_item_tiles=max_item_tiles or 0, partition=partition)
         else:
             self.shard = plan
+        # heads whose Q/K/V this rank reads (about H / world of them for "heads")
+        self.heads = self.shard.shard_heads() if self.shard is not plan else tuple(range(plan.n_heads))
+        self._inputs = None
         self.out = torch.empty(shape, dtype=torch.bfloat16, device=device)
         off = nat.c_int64(0)
         buf = (nat.c_uint8 * 64)()
@@ -110,14 +114,27 @@ class PeerShardedLayer:
         return self.out
 
     def e2e(self, hq, hk, hv, hout, groups=None):
-        """End-to-end step from pinned host buffers: H2D, fused shard kernel
-        (rows land in every rank's O), D2H of the full O."""
-        q = hq.to(self.device, non_blocking=True)
-        k = hk.to(self.device, non_blocking=True)
-        v = hv.to(self.device, non_blocking=True)
-        out = self(q, k, v)
-        hout.copy_(out, non_blocking=True)
+        """End-to-end step from pinned host buffers: H2D of the heads this
+        rank reads, the fused shard kernel (rows land in every rank's O), D2H
+        of those heads of O (the ranks' head sets cover every head)."""
+        import torch
+
+        if self._inputs is None or self._inputs[0].shape != hq.shape:
+            self._inputs = [torch.empty(hq.shape, dtype=hq.dtype, device=self.device) for _ in range(3)]
+        for src, dst in zip((hq, hk, hv), self._inputs):
+            for h in self.heads:
+                dst[:, h].copy_(src[:, h], non_blocking=True)
+        out = self(*self._inputs)
+        for h in self.heads:
+            hout[:, h].copy_(out[:, h], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
         return hout
+
+    def e2e_bytes(self, shape) -> tuple[int, int]:
+        """(H2D, D2H) bytes of this rank's e2e step for bf16 [B, H, N, d] tensors."""
+        B, _, N, d = shape
+        h = len(self.heads)
+        return 3 * B * h * N * d * 2, B * h * N * d * 2
 
     def close(self):
         for p, o in self._opened:

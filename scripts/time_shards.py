@@ -43,14 +43,17 @@ for pol in policies:
     for world in (2, 4, 8):
         times = []
         for r in range(world):
+            part = "items"
             if pol == "auto":
                 cap = 0
+            elif pol == "heads":  # contiguous head ranges, split cap chosen by the planner
+                cap, part = 0, "heads"
             elif pol == "none":
                 cap = -1
             else:  # "divN": cap = mean per-SM load / N
                 per_sm = plan.shard(world, r, max_item_tiles=-1).info.computed_tiles / 2 / 148
                 cap = max(32, int(per_sm / float(pol[3:])))
-            sh = plan.shard(world, r, max_item_tiles=cap)
+            sh = plan.shard(world, r, max_item_tiles=cap, partition=part)
             rows = max(1, len(sh.shard_rows()[0]))
             packed = torch.empty(rows, d, dtype=torch.bfloat16, device="cuda")
             times.append(timed(lambda: sh.forward(q, k, v, packed, head_dim=d), reps=3))

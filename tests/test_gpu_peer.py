@@ -54,6 +54,15 @@ def _worker(rank, world, port, path, d):
             out = layer(q, k, v)
             torch.cuda.synchronize()
             oks.append(bool(torch.equal(out, ref)))
+        # end to end: each rank copies in its own head range, copies out that range of O
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        hout = torch.full(q.shape, float("nan"), dtype=torch.bfloat16).pin_memory()
+        layer.e2e(hq, hk, hv, hout)
+        hs = list(layer.heads)
+        oks.append(bool(torch.equal(hout[:, hs], ref[:, hs].cpu())))
+        sets = [None] * world
+        dist.all_gather_object(sets, hs)
+        oks.append(set().union(*map(set, sets)) == set(range(len(specs))))
         dist.barrier()
         layer.close()
         torch.save({"ok": oks}, f"{path}.{rank}")

@@ -200,12 +200,36 @@ def test_schedule_hunyuan_efficiency():
     assert abs(plan.dense_flops(128) / 1e12 - 174.174) < 0.01
 
 
-def test_shards_partition_rows():
+@pytest.mark.parametrize("partition", ["items", "heads"])
+def test_shards_partition_rows(partition):
     layout = S.TokenLayout(40, 3, 150, 64)
     plan = S.LayerPlan.from_specs([S.full_spec(), S.diagonal_spec(1), S.skip_spec()], layout)
     for world in (1, 2, 3, 8):
         owned = []
         for r in range(world):
-            heads, toks = plan.shard(world, r).shard_rows()
+            heads, toks = plan.shard(world, r, partition=partition).shard_rows()
             owned += [(int(h), int(t)) for h, t in zip(heads, toks) if h >= 0]
         assert sorted(owned) == [(h, t) for h in range(3) for t in range(layout.total_tokens)]
+
+
+def test_head_partition_is_balanced_and_head_local():
+    """SVD_PARTITION_HEADS (McNaughton over an interleaved head sequence): the
+    ranks' head sets cover every head, at most world - 1 heads are shared
+    (split by query range), every rank reads about H / world heads, and the
+    issued tiles stay within a few percent of an even split (HunyuanVideo mix)."""
+    layout = S.TokenLayout(256, 33, 3600, 64)
+    asg = ([S.full_spec()] * 6 + [S.skip_spec()] + [S.diagonal_spec(1)] * 6 + [S.multi_diagonal_spec()] * 6
+           + [S.vertical_stripe_spec(stripes=(5 + 37 * i, 900 + 101 * i)) for i in range(5)])
+    plan = S.plan_for_assignment(asg, layout)
+    for world in (2, 4, 8):
+        shards = [plan.shard(world, r, n_sms=148, partition="heads") for r in range(world)]
+        sets = [set(s.shard_heads()) for s in shards]
+        assert set().union(*sets) == set(range(len(asg)))
+        assert sum(len(x) for x in sets) - len(asg) <= world - 1  # only boundary heads are shared
+        tiles = [s.info.computed_tiles for s in shards]
+        assert max(tiles) <= 1.03 * sum(tiles) / world
+        assert max(len(x) for x in sets) <= 2 * len(asg) // world + 2
+        items_sets = [plan.shard(world, r, n_sms=148).shard_heads() for r in range(world)]
+        assert max(len(x) for x in sets) < max(len(x) for x in items_sets)  # vs LPT over items
+    with pytest.raises(S.ConfigError):
+        plan.shard(2, 0, partition="rows")
