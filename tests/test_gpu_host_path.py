@@ -102,3 +102,26 @@ def test_output_head_map_and_zero_copy(monkeypatch):
     monkeypatch.setattr(A, "HOST_ZERO_COPY", True)
     got = S.fused_layer_attention(hq, hk, hv, groups)
     assert torch.equal(got, want) and torch.equal(got, ref.cpu())
+
+
+@pytest.mark.parametrize("block", [32, 96])
+def test_numpy_path_fine_blocks_match_device_path(block):
+    """float32 NumPy in/out (the reference's types) runs the chunked host
+    pipeline — head-subset plans (svd_plan_subset) incl. their FINE mask
+    tables for block sizes off the 64-token grain — and gives the device
+    path's bf16 result exactly."""
+    import numpy as np
+    import torch
+
+    lay = S.TokenLayout(37, 5, 200, block)
+    g = S.block_grid(lay)
+    specs = [S.diagonal_spec(1), S.full_spec(), S.skip_spec(), S.multi_diagonal_spec(period=3),
+             S.vertical_stripe_spec(stripes=(1, g.n_blocks - 2)), S.diagonal_spec(2)]
+    groups = S.group_heads(specs, g)
+    rng = np.random.default_rng(block)
+    q, k, v = (rng.standard_normal((1, len(specs), lay.total_tokens, 64), dtype=np.float32) for _ in range(3))
+    got = S.fused_layer_attention(q, k, v, groups)
+    assert got.dtype == np.float32
+    dev = S.fused_layer_attention(*(torch.from_numpy(x).cuda() for x in (q, k, v)), groups)
+    np.testing.assert_array_equal(got, dev.float().cpu().numpy())
+    assert not got[:, 2].any()
