@@ -443,6 +443,28 @@ def run_ours(args):
                               "bf16 on the host cores chunk by chunk into pinned staging, same pipeline")}
         del nq, nk, nv
 
+    # the offline search's per-layer step on this layer:
+    # stripe calibration (block_key_mass) and the four-candidate evaluation
+    search_step = None
+    if world == 1 and not args.no_dense:
+        from paper_2506_03065_b200.calibrate import CandidateEvaluator, block_key_mass
+
+        grid = S.block_grid(layout)
+        ev = CandidateEvaluator(grid, S.SearchParams())
+        ev.evaluate(q, k, v)  # first call builds the candidate plans
+        a0, a1, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a0.record(stream)
+        block_key_mass(q, k, grid)
+        a1.record(stream)
+        ev.evaluate(q, k, v)
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        search_step = {"block_key_mass_ms": round(a0.elapsed_time(a1), 2),
+                       "candidate_evaluation_ms": round(a1.elapsed_time(b1), 2),
+                       "what": "calibrate.block_key_mass (two tcgen05 passes) and "
+                               "CandidateEvaluator.evaluate (stripe calibration + FULL / diagonal / "
+                               "multi-diagonal / stripe candidates + per-head fp64 MSE), search.py:334-372"}
+
     # dense sm_100a baseline on the same GPU: every head FULL through the same kernel
     dense_ms = None
     if not args.no_dense and world == 1:
@@ -529,6 +551,7 @@ def run_ours(args):
                      if mgpu == "p2p" else "per rank: full H2D, shard kernel, NCCL all-gather, full D2H"),
         },
         "e2e_reference_types": numpy_e2e,
+        "search_step": search_step,
         "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),
         "clocks": clock,
     }
