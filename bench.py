@@ -291,6 +291,50 @@ def library_dense(q, k, v, dev, reps: int = 3):
     return {"backend": None, "ms": None, "error": last}
 
 
+def _numpy_e2e(S, hq, hk, hv, groups, e2e_bytes):
+    """The reference's own call with its own types: float32 NumPy in, float32
+    NumPy out (attention.py:186-212), wall clock per call (1 GPU)."""
+    try:
+        nq, nk, nv = (t.float().numpy() for t in (hq, hk, hv))
+        S.fused_layer_attention(nq, nk, nv, groups)
+        walls = []
+        for _ in range(3):
+            w0 = time.perf_counter()
+            S.fused_layer_attention(nq, nk, nv, groups)
+            walls.append(round((time.perf_counter() - w0) * 1e3, 2))
+        numpy_e2e = {"ms_per_layer": min(walls), "wall_ms_steps": walls,
+                     "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1],
+                     "path": ("fused_layer_attention(float32 NumPy q/k/v) -> float32 NumPy: converted to "
+                              "bf16 on the host cores chunk by chunk into pinned staging, same pipeline")}
+        del nq, nk, nv
+        return numpy_e2e
+    except Exception as exc:  # informational extra: never sink the bench line
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
+def _search_step(S, layout, q, k, v, stream, dev):
+    """The offline search's per-layer step on the bench layer."""
+    import torch
+
+    from paper_2506_03065_b200.calibrate import CandidateEvaluator, block_key_mass
+
+    grid = S.block_grid(layout)
+    ev = CandidateEvaluator(grid, S.SearchParams())
+    ev.evaluate(q, k, v)  # first call builds the candidate plans
+    a0, a1, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    a0.record(stream)
+    block_key_mass(q, k, grid)
+    a1.record(stream)
+    ev.evaluate(q, k, v)
+    b1.record(stream)
+    torch.cuda.synchronize(dev)
+    return {"block_key_mass_ms": round(a0.elapsed_time(a1), 2),
+            "candidate_evaluation_ms": round(a1.elapsed_time(b1), 2),
+            "what": "calibrate.block_key_mass (two tcgen05 passes) and "
+                    "CandidateEvaluator.evaluate (stripe calibration + FULL / diagonal / "
+                    "multi-diagonal / stripe candidates + per-head fp64 MSE), search.py:334-372"}
+
+
 def init_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -430,40 +474,16 @@ def run_ours(args):
     # NumPy out (attention.py:186-212), wall clock per call (1 GPU)
     numpy_e2e = None
     if world == 1:
-        nq, nk, nv = (t.float().numpy() for t in (hq, hk, hv))
-        S.fused_layer_attention(nq, nk, nv, groups)
-        walls = []
-        for _ in range(3):
-            w0 = time.perf_counter()
-            S.fused_layer_attention(nq, nk, nv, groups)
-            walls.append(round((time.perf_counter() - w0) * 1e3, 2))
-        numpy_e2e = {"ms_per_layer": min(walls), "wall_ms_steps": walls,
-                     "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1],
-                     "path": ("fused_layer_attention(float32 NumPy q/k/v) -> float32 NumPy: converted to "
-                              "bf16 on the host cores chunk by chunk into pinned staging, same pipeline")}
-        del nq, nk, nv
+        numpy_e2e = _numpy_e2e(S, hq, hk, hv, groups, e2e_bytes)
 
     # the offline search's per-layer step on this layer:
     # stripe calibration (block_key_mass) and the four-candidate evaluation
     search_step = None
     if world == 1 and not args.no_dense:
-        from paper_2506_03065_b200.calibrate import CandidateEvaluator, block_key_mass
-
-        grid = S.block_grid(layout)
-        ev = CandidateEvaluator(grid, S.SearchParams())
-        ev.evaluate(q, k, v)  # first call builds the candidate plans
-        a0, a1, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        a0.record(stream)
-        block_key_mass(q, k, grid)
-        a1.record(stream)
-        ev.evaluate(q, k, v)
-        b1.record(stream)
-        torch.cuda.synchronize(dev)
-        search_step = {"block_key_mass_ms": round(a0.elapsed_time(a1), 2),
-                       "candidate_evaluation_ms": round(a1.elapsed_time(b1), 2),
-                       "what": "calibrate.block_key_mass (two tcgen05 passes) and "
-                               "CandidateEvaluator.evaluate (stripe calibration + FULL / diagonal / "
-                               "multi-diagonal / stripe candidates + per-head fp64 MSE), search.py:334-372"}
+        try:
+            search_step = _search_step(S, layout, q, k, v, stream, dev)
+        except Exception as exc:  # informational extra: never sink the bench line
+            search_step = {"error": f"{type(exc).__name__}: {exc}"}
 
     # dense sm_100a baseline on the same GPU: every head FULL through the same kernel
     dense_ms = None
