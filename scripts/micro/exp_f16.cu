@@ -4,6 +4,12 @@
 //   V0  fp32 ex2 per element (MUFU.EX2 x2 per pair)            — the kernel today
 //   V1  x -> f16x2, ex2.approx.f16x2 (one MUFU per pair), f16 -> f32 -> bf16x2
 //   V2  x -> bf16x2, ex2.approx.ftz.bf16x2 (one MUFU per pair), result is P
+//   V3  fp32 ex2 + F2FP pack, no row sums          (which ops share the MUFU's pipe?)
+//   V4  fp32 ex2 + fp32 FADD2 row sums, no pack
+//   V5  fp32 ex2 only (results xor-folded)
+//   V6  fp32 ex2 + F2FP pack + rounded row sums by unpacking the packed pair
+//       (bf16 -> f32 is a 16-bit shift: SHF / LOP + one FADD2) instead of FHADD.BF16
+//   V7  as V6, the sums taken after all 16 pairs of the chunk are packed
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -53,6 +59,23 @@ __global__ void __launch_bounds__(256, 1) k_exp(int iters, const float* in, uint
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float2 xv = ptx::ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sl, nm);
+        if (V == 6) {
+          pk[i] = ptx::pack_bf16(ptx::ex2(xv.x), ptx::ex2(xv.y));
+          acc[i & 3] = ptx::fadd2(acc[i & 3], make_float2(__uint_as_float(pk[i] << 16),
+                                                          __uint_as_float(pk[i] & 0xFFFF0000u)));
+          continue;
+        }
+        if (V == 7) {
+          pk[i] = ptx::pack_bf16(ptx::ex2(xv.x), ptx::ex2(xv.y));
+          continue;
+        }
+        if (V >= 3) {
+          const float2 pv = make_float2(ptx::ex2(xv.x), ptx::ex2(xv.y));
+          if (V == 3) pk[i] = ptx::pack_bf16(pv.x, pv.y);
+          else if (V == 4) { acc[i & 3] = ptx::fadd2(acc[i & 3], pv); pk[i] = 0; }
+          else pk[i] = __float_as_uint(pv.x) ^ __float_as_uint(pv.y);
+          continue;
+        }
         if (V == 0) {
           pk[i] = ptx::pack_bf16(ptx::ex2(xv.x), ptx::ex2(xv.y));
         } else if (V == 1) {
@@ -62,6 +85,12 @@ __global__ void __launch_bounds__(256, 1) k_exp(int iters, const float* in, uint
           pk[i] = ex2_bf16x2(ptx::pack_bf16(xv.x, xv.y));
         }
         ptx::acc_bf16x2(acc[i & 3], pk[i]);
+      }
+      if (V == 7) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          acc[i & 3] = ptx::fadd2(acc[i & 3], make_float2(__uint_as_float(pk[i] << 16),
+                                                          __uint_as_float(pk[i] & 0xFFFF0000u)));
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc_pk ^= pk[i];
@@ -100,6 +129,11 @@ int main() {
     run<0>(sms, threads, in, sink, cyc);
     run<1>(sms, threads, in, sink, cyc);
     run<2>(sms, threads, in, sink, cyc);
+    run<3>(sms, threads, in, sink, cyc);
+    run<4>(sms, threads, in, sink, cyc);
+    run<5>(sms, threads, in, sink, cyc);
+    run<6>(sms, threads, in, sink, cyc);
+    run<7>(sms, threads, in, sink, cyc);
   }
   return 0;
 }
