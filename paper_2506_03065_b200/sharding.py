@@ -2,12 +2,15 @@
 
 Heads are independent (attention.py:211 writes only out[:, idx]) and so are
 query blocks within a head (attention.py:81-97).  The plan's work items —
-(head, four query segments) with their KV tile lists — are split over ranks
-by LPT on tile cost (svd_plan_shard), so FULL heads are divided by query
-range instead of being indivisible.  Each rank writes its rows into a packed
-buffer; one NCCL all-gather over NVLink reassembles them and the unpack
-kernel scatters the rows back into O[B=1, H, N, d].  Q/K/V are replicated on
-every rank, as layer_qkv produces them (model.py:372-391).
+(head, four query segments) with their KV tile lists — are dealt to ranks
+balancing tile cost (svd_plan_shard_ex): by default head-locally (each rank
+holds ~H/N heads, at most its two boundary heads split by query range), or
+by LPT over all items.  PeerShardedLayer (default) fuses the reassembly into
+the kernel: each rank's shard stores its rows into every rank's O over peer
+memory.  HeadShardedLayer writes packed rows that one NCCL all-gather plus
+the unpack kernel scatter back into O[B=1, H, N, d].  Device-resident Q/K/V
+are taken as given on every rank (as layer_qkv produces them,
+model.py:372-391); from host buffers a rank copies in only its own heads.
 """
 
 from __future__ import annotations
