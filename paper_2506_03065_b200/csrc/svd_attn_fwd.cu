@@ -51,6 +51,15 @@ constexpr uint32_t kTmemCols = 512;
 #ifndef SVD_SUM_AFTER_ST
 #define SVD_SUM_AFTER_ST 1
 #endif
+// P handed to the PV MMA in 32-key quarters instead of 64-key halves
+// (bit 0: d=64, bit 1: d=128).  d=64: the PV starts after the first 32 keys'
+// exps (CogVideoX -1.7%); d=128: +6% (the extra st-waits lengthen the
+// softmax, which is the tensor pipe's feeder there)
+#ifndef SVD_P_QUARTERS
+#define SVD_P_QUARTERS 1
+#endif
+template <int D>
+constexpr bool kPQuarters = (SVD_P_QUARTERS >> (D == 128 ? 1 : 0)) & 1;
 #ifndef SVD_SUM_ROUNDED
 #define SVD_SUM_ROUNDED 1
 #endif
@@ -79,7 +88,9 @@ struct KCfg {
   static constexpr int kBarS = kBarVE + kVSt;
   static constexpr int kBarP0 = kBarS + 2;
   static constexpr int kBarP1 = kBarP0 + 2;
-  static constexpr int kBarO = kBarP1 + 2;
+  static constexpr int kBarP2 = kBarP1 + 2;  // P in quarters (SVD_P_QUARTERS)
+  static constexpr int kBarP3 = kBarP2 + 2;
+  static constexpr int kBarO = kBarP3 + 2;
   static constexpr int kNumBars = kBarO + 2;
   static constexpr int kOffTmemSlot = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmemSlot + 16 + 1024;  // + alignment slack
@@ -278,6 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(bar(C::kBarS + x), 1);
       ptx::mbar_init(bar(C::kBarP0 + x), 128);
       ptx::mbar_init(bar(C::kBarP1 + x), 128);
+      ptx::mbar_init(bar(C::kBarP2 + x), 128);
+      ptx::mbar_init(bar(C::kBarP3 + x), 128);
       ptx::mbar_init(bar(C::kBarO + x), 1);
     }
     ptx::fence_barrier_init();
@@ -386,6 +399,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tn = 0;
         (void)tn;
         auto issue_pv = [&](int x, int vs, int j) {
+          if constexpr (kPQuarters<D>) {
+            // P handed over in 32-key quarters: two K=16 MMAs per quarter
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              ptx::mbar_wait(bar(C::kBarP0 + 2 * qq + x), j & 1);
+              ptx::tc_fence_after();
+              const uint32_t vlo = ptx::sw128_lo(sb + C::kOffV + vs * C::kTileBytes, C::kSlabBytes);
+#pragma unroll
+              for (int k2 = 0; k2 < 2; ++k2) {
+                const int kk = qq * 2 + k2;
+                mma_t(tb + C::col_o(x), tb + C::col_p(x) + kk * 8, vlo + ((kk * 2048) >> 4), hi, id_pv,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            return;
+          }
           TRACE(2, tn, j, 30 + x);
           ptx::mbar_wait(bar(C::kBarP0 + x), j & 1);
           TRACE(2, tn, j, 40 + x);
@@ -585,7 +614,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) ptx::acc_bf16x2(acc[i & 3], pk[i]);
       }
-      if (c == 1 || c == 3) {
+      if (kPQuarters<D>) {
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar(C::kBarP0 + 2 * c + x));
+      } else if (c == 1 || c == 3) {
         // hand P over in two 64-key halves: PV on the first half overlaps
         // the exps of the second
         ptx::tmem_wait_st();
