@@ -60,6 +60,12 @@ constexpr uint32_t kTmemCols = 512;
 #endif
 template <int D>
 constexpr bool kPQuarters = (SVD_P_QUARTERS >> (D == 128 ? 1 : 0)) & 1;
+// two-part P handoff (d=128): the first part ends after 32-key chunk
+// SVD_P_FIRST (0..2).  0 — PV starts after the first 32 keys, the rest follows
+// as one part: -0.5% vs even halves (1), +1% for 2
+#ifndef SVD_P_FIRST
+#define SVD_P_FIRST 0
+#endif
 #ifndef SVD_SUM_ROUNDED
 #define SVD_SUM_ROUNDED 1
 #endif
@@ -389,9 +395,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // O_X += P_X V_j, keys [64*half, 64*half + 64): four K=16 steps
         auto issue_pv_half = [&](int x, int vs, int half, bool acc) {
           const uint32_t vlo = ptx::sw128_lo(sb + C::kOffV + vs * C::kTileBytes, C::kSlabBytes);
+          constexpr int kSplit = 2 * (SVD_P_FIRST + 1);  // K=16 steps in the first part
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const int kk = half * 4 + k4;
+          for (int kk = half ? kSplit : 0; kk < (half ? 8 : kSplit); ++kk) {
             mma_t(tb + C::col_o(x), tb + C::col_p(x) + kk * 8, vlo + ((kk * 2048) >> 4), hi, id_pv,
                   (acc || kk > 0) ? 1u : 0u);
           }
@@ -618,14 +624,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar(C::kBarP0 + 2 * c + x));
-      } else if (c == 1 || c == 3) {
-        // hand P over in two 64-key halves: PV on the first half overlaps
-        // the exps of the second
+      } else if (c == SVD_P_FIRST || c == 3) {
+        // hand P over in two parts: PV on the first part overlaps the exps
+        // of the rest
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(bar(c == 1 ? C::kBarP0 + x : C::kBarP1 + x));
+        ptx::mbar_arrive(bar(c == SVD_P_FIRST ? C::kBarP0 + x : C::kBarP1 + x));
 #ifdef SVD_TRACE
-        if (tr) TRACE(x, tn, j, c == 1 ? 6 : 2);  // P half 0 / 1 handed over
+        if (tr) TRACE(x, tn, j, c == SVD_P_FIRST ? 6 : 2);  // P part 0 / 1 handed over
 #endif
       }
     }
