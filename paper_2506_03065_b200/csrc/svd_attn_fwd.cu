@@ -17,7 +17,9 @@
 //   warps 8-11   softmax/epilogue for Q tile B
 // Per KV tile j the issuer runs, ping-ponging between the two Q tiles,
 //   S_X = Q_X K_j^T          (SS MMA, M=128 N=128 K=d, fp32 in TMEM)
-//   O_X += P_X V_j           (TS MMA: P bf16 from TMEM, V MN-major in smem)
+//   O_X += P_X V_j           (TS MMA: P bf16 from TMEM, V MN-major in smem;
+//                             issued per part as P is handed over: keys 0-31
+//                             then 32-127 at d=128, 32-key quarters at d=64)
 // while the softmax warpgroups turn S_X into P_X (masking, running max with
 // lazy rescale of O, exp2 — at d=128 3/8 of it on the FMA pipe — bf16 P,
 // rounded row sums) — so one tile's exps overlap the other tile's MMAs.
