@@ -51,11 +51,17 @@ CONFIGS = {
 }
 
 
+UNIT = "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)"
+MODE_LABELS = {0: "full", 1: "skip", 2: "diagonal", 3: "multi_diagonal", 4: "vertical_stripe"}
+
+
 def assignment_for(cfg, S):
     """Per-head specs for a config: the paper-derived mode mix with distinct
-    stripe columns per stripe head (seeded), in a fixed shuffled head order."""
-    layout = S.TokenLayout(*cfg["layout"])
-    nb = layout.n_blocks
+    stripe columns per stripe head (seeded), in a fixed shuffled head order.
+    S supplies the spec constructors: the product package (GPU arm) or the
+    oracle (CPU arms) — both give the same table."""
+    text, frames, tpf, bs = cfg["layout"]
+    nb = -(-(text + frames * tpf) // bs)
     if cfg["mix"] is None:  # config 1 table
         return [S.full_spec(), S.diagonal_spec(1), S.multi_diagonal_spec(),
                 S.vertical_stripe_spec(stripes=(0, 7)), S.skip_spec(), S.diagonal_spec(1),
@@ -67,6 +73,33 @@ def assignment_for(cfg, S):
              [S.multi_diagonal_spec()] * md + [S.vertical_stripe_spec(stripes=c) for c in stripes])
     order = rng.permutation(len(specs))
     return [specs[i] for i in order]
+
+
+def config_dict(cfg, density: float, parallelism: str) -> dict:
+    """The workload description both arms print (same keys, same values)."""
+    H, d = cfg["heads"], cfg["d"]
+    n = cfg["layout"][0] + cfg["layout"][1] * cfg["layout"][2]
+    return {
+        "workload": cfg["name"],
+        "layout": {"text_tokens": cfg["layout"][0], "frames": cfg["layout"][1],
+                   "tokens_per_frame": cfg["layout"][2], "block_size": cfg["layout"][3]},
+        "tokens": n, "heads": H, "head_dim": d, "batch": 1,
+        "mode_mix_F_S_D_MD_VS": cfg["mix"],
+        "density": round(density, 4),
+        "parallelism": parallelism,
+        "l2": (("inputs 3 x %.0f MB bf16 > 126 MB L2: no flush" if H * n * d * 2 * 3 > 126e6 else
+                "inputs 3 x %.1f MB bf16 fit in L2 (a parity-size case, not the metric's config)")
+               % (H * n * d * 2 / 1e6)),
+    }
+
+
+def _oracle():
+    """The CPU oracle — imported only by the CPU legs (cpu_baseline, the
+    reference arm and the parity checker), never by the measured GPU path."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import svdit_oracle as O
+
+    return O
 
 
 # ----------------------------------------------------------------- clocks
@@ -154,16 +187,14 @@ def _cpu_init(layout, d, mode_specs):
     """Spawned-worker initializer: the oracle, the grid, seeded Q/K/V (one
     head at full N) and the per-mode masks — rebuilt in every worker, so the
     pool never inherits the parent's CUDA / BLAS thread state."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import svdit_oracle as O
-
+    O = _oracle()
     og = O.block_grid(*layout)
     rng = np.random.default_rng(0)
     _CPU.update(O=O, grid=og,
                 q=rng.standard_normal((1, 1, og.n, d), dtype=np.float32),
                 k=rng.standard_normal((1, 1, og.n, d), dtype=np.float32),
                 v=rng.standard_normal((1, 1, og.n, d), dtype=np.float32),
-                active={m: O.build_mask(sp, og) for m, sp in mode_specs.items()})
+                active={m: O.build_mask(O.Spec(*sp), og) for m, sp in mode_specs.items()})
 
 
 def _cpu_worker(args):
@@ -195,72 +226,143 @@ def _cpu_worker(args):
     return done, time.perf_counter() - t0, nq
 
 
-def cpu_baseline(cfg, S, budget_s: float = 15.0) -> dict:
-    """Time the reference algorithm (fp64 streaming online softmax, the oracle
-    port of attention.py:57-98) on this host's cores over a bounded sample of
-    query blocks of one head per distinct mode at full N, and extrapolate to
-    the whole layer by active FLOPs per mode.  Query blocks are independent
-    (attention.py:81-97), so one forked worker per core runs the unchanged
-    per-block algorithm with one BLAS thread each."""
-    import multiprocessing as mp
+class CpuBaseline:
+    """The reference algorithm (fp64 streaming online softmax, the oracle port
+    of attention.py:57-98) on this host's cores: bounded samples of query
+    blocks of one head per distinct mode at full N, extrapolated to the whole
+    layer by active FLOPs per mode.  Query blocks are independent
+    (attention.py:81-97), so one spawned worker per core runs the unchanged
+    per-block algorithm with one BLAS thread each.  The worker pool is built
+    once and reused by every sample."""
 
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import svdit_oracle as O
+    def __init__(self, cfg):
+        import multiprocessing as mp
 
-    text, frames, tpf, bs = cfg["layout"]
-    og = O.block_grid(text, frames, tpf, bs)
-    n, d = og.n, cfg["d"]
-    specs = assignment_for(cfg, S)
-    rng = np.random.default_rng(1)
-    per_mode = {}
-    for spec in specs:
-        per_mode.setdefault(int(spec.mode), spec)
-    modes = [m for m in per_mode if m != 1]
-    workers = max(1, os.cpu_count() or 1)
-    slice_s = budget_s / max(1, len(modes))
-    total_flops_layer = 0.0
-    total_time_layer = 0.0
-    sampled = []
-    ctx = mp.get_context("spawn")
-    env_blas = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
-    for k in env_blas:  # spawned workers start with single-threaded BLAS
-        os.environ[k] = "1"
-    try:
-        pool = ctx.Pool(workers, initializer=_cpu_init,
-                        initargs=(cfg["layout"], d, {m: per_mode[m] for m in modes}))
-    finally:
-        for k, val in env_blas.items():
-            if val is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = val
-    with pool:
-        for m in modes:
-            heads_m = sum(1 for s in specs if int(s.mode) == m)
-            flops_mode = sum(4.0 * d * O.active_pairs(O.build_mask(s, og), og.bounds)
-                             for s in specs if int(s.mode) == m)
-            order = rng.permutation(og.n_blocks)
-            shares = [order[w::workers] for w in range(workers)]
-            res = pool.map(_cpu_worker, [(m, sh, slice_s) for sh in shares])
+        O = _oracle()
+        self.cfg = cfg
+        self.og = og = O.block_grid(*cfg["layout"])
+        self.d = cfg["d"]
+        self.specs = assignment_for(cfg, O)
+        per_mode = {}
+        for spec in self.specs:
+            per_mode.setdefault(int(spec.mode), spec)
+        self.modes = [m for m in per_mode if m != O.SKIP]
+        self.heads = {m: sum(1 for s in self.specs if int(s.mode) == m) for m in self.modes}
+        pairs = {m: 0.0 for m in self.modes}
+        dense_pairs = float(og.n) * float(og.n)
+        for s in self.specs:  # masks are bit-exact with the plan builder's
+            if int(s.mode) != O.SKIP:
+                pairs[int(s.mode)] += O.active_pairs(O.build_mask(s, og), og.bounds)
+        self.flops = {m: 4.0 * self.d * pairs[m] for m in self.modes}
+        self.density = sum(pairs.values()) / (dense_pairs * len(self.specs))
+        self.workers = max(1, os.cpu_count() or 1)
+        self.rng = np.random.default_rng(1)
+        ctx = mp.get_context("spawn")
+        env_blas = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+        for k in env_blas:  # spawned workers start with single-threaded BLAS
+            os.environ[k] = "1"
+        try:
+            self.pool = ctx.Pool(self.workers, initializer=_cpu_init,
+                                 initargs=(cfg["layout"], self.d,
+                                           {m: tuple(per_mode[m]) for m in self.modes}))
+        finally:
+            for k, val in env_blas.items():
+                if val is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = val
+
+    def sample(self, budget_s: float) -> dict:
+        """One bounded sample (~budget_s of wall time on all workers)."""
+        og, n, d = self.og, self.og.n, self.d
+        slice_s = budget_s / max(1, len(self.modes))
+        total_flops, total_time, sampled = 0.0, 0.0, []
+        w0 = time.perf_counter()
+        for m in self.modes:
+            order = self.rng.permutation(og.n_blocks)
+            shares = [order[w::self.workers] for w in range(self.workers)]
+            res = self.pool.map(_cpu_worker, [(m, sh, slice_s) for sh in shares])
             done = sum(r[0] for r in res)
             wall = max(r[1] for r in res)
             nq = sum(r[2] for r in res)
             rate = done / wall
-            total_flops_layer += flops_mode
-            total_time_layer += flops_mode / rate
-            sampled.append(f"{S.Mode(m).label}:{nq}qb/{heads_m}h {rate / 1e9:.1f}GF/s")
-    dense = 4.0 * n * n * d * cfg["heads"]
-    return {
-        "value": dense / total_time_layer / 1e12,
-        "unit": "TFLOP/s (dense-equivalent)",
-        "ms_per_layer": total_time_layer * 1e3,
-        "active_gflops_per_s": total_flops_layer / total_time_layer / 1e9,
-        "cores": workers,
-        "kind": "port",
-        "sample": (f"fp64 NumPy oracle (attention.py:57-98 restated), 1 head per mode at full N={n}, "
-                   f"random query blocks for ~{slice_s:.0f}s each on {workers} worker processes x 1 BLAS "
-                   f"thread [{'; '.join(sampled)}], extrapolated by active FLOPs"),
-    }
+            total_flops += self.flops[m]
+            total_time += self.flops[m] / rate
+            sampled.append(f"{MODE_LABELS[m]}:{nq}qb/{self.heads[m]}h {rate / 1e9:.1f}GF/s")
+        wall_ms = (time.perf_counter() - w0) * 1e3
+        dense = 4.0 * n * n * d * self.cfg["heads"]
+        return {
+            "value": dense / total_time / 1e12,
+            "unit": UNIT,
+            "ms_per_layer": total_time * 1e3,
+            "extrapolated": True,
+            "sample_wall_ms": round(wall_ms, 1),
+            "active_gflops_per_s": total_flops / total_time / 1e9,
+            "cores": self.workers,
+            "kind": "port",
+            "sample": (f"fp64 NumPy oracle (attention.py:57-98 restated), 1 head per mode at full N={n}, "
+                       f"random query blocks for ~{slice_s:.1f}s each on {self.workers} worker processes x "
+                       f"1 BLAS thread [{'; '.join(sampled)}], layer time extrapolated by active FLOPs"),
+        }
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(cfg, budget_s: float = 15.0) -> dict:
+    cb = CpuBaseline(cfg)
+    try:
+        return cb.sample(budget_s)
+    finally:
+        cb.close()
+
+
+def oracle_parity(cfg, q, k, v, out, specs, per_head: int = 4) -> dict:
+    """Checker (outside the timed region): sampled output rows of the bench
+    layer against the oracle — every head, query blocks chosen to cover the
+    text / forced rows, a frame-border (mixed) block, an ordinary block and
+    the partial tail — max-abs / mean-abs over the sampled elements, the
+    north_star bar being 2e-2 / 2e-3 (bf16 output vs the fp32 reference)."""
+    import torch
+
+    O = _oracle()
+    og = O.block_grid(*cfg["layout"])
+    nb = og.n_blocks
+    rng = np.random.default_rng(7)
+    forced = np.flatnonzero(og.forced)
+    mixed = np.flatnonzero(og.mixed & ~og.has_text)
+    plain = np.flatnonzero(~og.forced[:-1])
+    t0 = time.perf_counter()
+    errs, n_el, rows = [], 0, 0
+    worst = 0.0
+    for h, spec in enumerate(specs):
+        picks = {int(nb - 1)}
+        if len(forced):
+            picks.add(int(forced[0]))
+        if len(mixed):
+            picks.add(int(rng.choice(mixed)))
+        while len(picks) < per_head:
+            picks.add(int(rng.choice(plain)))
+        qbs = sorted(picks)
+        sel = np.concatenate([np.arange(og.bounds[b], og.bounds[b + 1]) for b in qbs])
+        got = out[:, h:h + 1, torch.as_tensor(sel, device=out.device)].float().cpu().numpy()
+        if int(spec.mode) == O.SKIP:
+            want = np.zeros_like(got)
+        else:
+            hq, hk, hv = (x[:, h:h + 1].float().cpu().numpy() for x in (q, k, v))
+            want = O.attention_rows(hq, hk, hv, O.build_mask(spec, og), og.bounds, qbs)
+        e = np.abs(got - want)
+        errs.append(float(e.sum()))
+        n_el += e.size
+        rows += len(sel)
+        worst = max(worst, float(e.max()))
+    return {"max_abs": worst, "mean_abs": sum(errs) / max(1, n_el), "tol_max_abs": 2e-2,
+            "tol_mean_abs": 2e-3, "ok": bool(worst <= 2e-2 and sum(errs) / max(1, n_el) <= 2e-3),
+            "rows_checked": rows, "heads_checked": len(specs), "seconds": round(time.perf_counter() - t0, 1),
+            "how": ("fp64 oracle rows (oracle.attention_rows, attention.py:57-98 semantics) for "
+                    f"{per_head} query blocks per head (text/forced, frame-border, ordinary, partial tail) "
+                    "of the bench's own inputs and mode mix, against the timed kernel's bf16 output")}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -407,8 +509,11 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    # the peer layer double-buffers O: call it without out= and keep the result
+    step = (lambda ev=None: layer(q, k, v, kernel_events=ev)) if mgpu == "p2p" else \
+        (lambda ev=None: layer(q, k, v, out, kernel_events=ev))
     for _ in range(args.warmup):
-        layer(q, k, v, out)
+        out = step()
     barrier()
     # kernel-only events around each fused launch (same stream) for the roofline
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -418,7 +523,7 @@ def run_ours(args):
         barrier()
         t0.record(stream)
         for i in range(args.steps):
-            layer(q, k, v, out, kernel_events=kev[i])
+            out = step(kev[i])
         t1.record(stream)
         barrier()
     ms = t0.elapsed_time(t1) / args.steps
@@ -460,9 +565,20 @@ def run_ours(args):
         e2e_bytes = layer.e2e_bytes((1, H, n, d))
     else:
         e2e_bytes = (3 * H * n * d * 2, H * n * d * 2)
+    # peer-memory bytes a rank's epilogue stores into the other ranks' O per
+    # step (p2p), or receives through the NCCL all-gather (nccl)
+    if world == 1:
+        link_bytes = 0
+    elif mgpu == "p2p":
+        link_bytes = layer.nvlink_bytes(d)
+    else:
+        link_bytes = (world - 1) * layer.max_rows * layer.tensor_dim * 2
     if world > 1:
         import torch.distributed as dist
 
+        lt = torch.tensor([float(link_bytes)], device=dev, dtype=torch.float64)
+        dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+        link_bytes = int(lt[0])
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt[0])
@@ -504,6 +620,13 @@ def run_ours(args):
         del dense_out
     dense_lib = library_dense(q, k, v, dev) if (not args.no_dense and world == 1) else None
 
+    # the checker: sampled rows of the timed output vs the oracle (not timed)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = oracle_parity(cfg, q, k, v, out, specs)
+        except Exception as exc:  # never sink the bench line; the gpu tests gate parity
+            parity = {"error": f"{type(exc).__name__}: {exc}"}
     if rank != 0:
         return
     peaks = measured_peaks()
@@ -513,7 +636,7 @@ def run_ours(args):
     line = {
         "metric": METRIC,
         "value": round(f_dense / (ms * 1e-3) / 1e12, 2),
-        "unit": "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)",
+        "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -523,19 +646,7 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (torch.randn Q/K/V, seed 1234)",
-        "config": {
-            "workload": cfg["name"],
-            "layout": {"text_tokens": cfg["layout"][0], "frames": cfg["layout"][1],
-                       "tokens_per_frame": cfg["layout"][2], "block_size": cfg["layout"][3]},
-            "heads": H, "head_dim": d, "batch": 1,
-            "mode_mix_F_S_D_MD_VS": cfg["mix"],
-            "density": round(f_active / f_dense, 4),
-            "parallelism": ({"p2p": f"head/q-range sharded x{world}, rows stored to every rank's O "
-                                    "from the kernel epilogue over peer memory",
-                             "nccl": f"head/q-range sharded x{world} + NCCL all-gather + unpack",
-                             "single": "1 GPU"}[mgpu]),
-            "l2": "inputs 3 x %.0f MB bf16 > 126 MB L2: no flush" % (H * n * d * 2 / 1e6),
-        },
+        "config": config_dict(cfg, f_active / f_dense, parallelism_label(mgpu, world)),
         "ms_per_layer": round(ms, 4),
         "active_tflops": round(f_active / (ms * 1e-3) / 1e12, 2),
         "kernel_ms": round(kms, 4),
@@ -547,18 +658,22 @@ def run_ours(args):
         "roofline": {
             "bound": "tensor",
             "achieved": round(achieved, 2),
-            "peak": peaks["bf16_sustained"],
+            "peak": peaks["bf16"],
             "unit": "TFLOP/s",
-            "frac": round(achieved / peaks["bf16_sustained"], 4),
+            "frac": round(achieved / peaks["bf16"], 4),
             "traffic": traffic,
-            "peak_kind": f"{peaks['source']} sustained cuBLAS bf16 (kernel timed inside a long loop)",
-            "frac_of_burst_peak": round(achieved / peaks["bf16"], 4),
+            "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed "
+                               "ncu --set full capture of this kernel on this config (profiles/ncu_summary.json), "
+                               "not measured in this run"),
+            "peak_kind": f"{peaks['source']} burst cuBLAS bf16 (each ~40 ms launch is timed on its own)",
+            "frac_of_sustained_peak": round(achieved / peaks["bf16_sustained"], 4),
+            "sustained_peak": peaks["bf16_sustained"],
             "algorithmic_flops_per_launch": f_active / world,
             "issued_tile_flops_per_launch": info.computed_tiles * 4.0 * 128 * 128 * d / world,
         },
         "e2e": {
             "value": round(f_dense / (e2e_ms * 1e-3) / 1e12, 2),
-            "unit": "TFLOP/s (effective, dense-equivalent)",
+            "unit": UNIT,
             "ms_per_layer": round(e2e_ms, 3),
             "wall_ms_steps": e2e_walls,
             "h2d_bytes_per_step": e2e_bytes[0],
@@ -572,41 +687,62 @@ def run_ours(args):
         },
         "e2e_reference_types": numpy_e2e,
         "search_step": search_step,
-        "gpu_launches": args.steps * (2 if mgpu == "nccl" else 1),
+        "nvlink_bytes_per_rank_per_step": link_bytes,
+        "gpu_launches": args.steps * (2 if mgpu in ("nccl", "p2p") and world > 1 else 1),
         "clocks": clock,
     }
+    line["parity"] = parity
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, S, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
 
 
+def parallelism_label(mgpu: str, world: int) -> str:
+    return {"p2p": f"head/q-range sharded x{world}, rows stored to every rank's O "
+                   "from the kernel epilogue over peer memory",
+            "nccl": f"head/q-range sharded x{world} + NCCL all-gather + unpack",
+            "single": "1 GPU"}[mgpu]
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm on the host cores (oracle port;
-    /root/reference is not available on the GPU box)."""
+    """--impl reference: the reference algorithm on the host cores (the oracle
+    port — /root/reference is not available on the GPU box).
+    Nothing from the product package is imported.  Each step is one bounded
+    sample of the layer (every non-SKIP mode at full N, ~budget seconds on all
+    cores); the layer time is extrapolated by active FLOPs and the line says
+    so.  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2506_03065_b200 as S
-
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     cfg = CONFIGS[args.config]
-    n = cfg["layout"][0] + cfg["layout"][1] * cfg["layout"][2]
-    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_baseline(cfg, S, budget_s=budget)
-    vals = [cpu_baseline(cfg, S, budget_s=budget) for _ in range(args.steps)]
+    budget = max(1.0, min(10.0, 120.0 / max(1, args.steps + args.warmup)))
+    cb = CpuBaseline(cfg)
+    try:
+        for _ in range(args.warmup):
+            cb.sample(budget)
+        vals = [cb.sample(budget) for _ in range(args.steps)]
+    finally:
+        cb.close()
     value = statistics.median(v["value"] for v in vals)
-    ms = statistics.median(v["ms_per_layer"] for v in vals)
-    cb = dict(vals[0])
-    cb["value"] = value
+    layer_ms = statistics.median(v["ms_per_layer"] for v in vals)
+    step_ms = statistics.mean(v["sample_wall_ms"] for v in vals)
+    base = dict(vals[0])
+    base["value"] = value
+    base["ms_per_layer"] = layer_ms
+    mgpu = "single" if world == 1 else os.environ.get("SVD_MULTI_GPU", "p2p")
     line = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)",
-        "impl": "reference", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "tokens": n, "heads": cfg["heads"], "head_dim": cfg["d"]},
-        "cpu_baseline": cb,
-        "e2e": {"value": value, "unit": "TFLOP/s (effective, dense-equivalent 4*N^2*d*H)",
-                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": value, "unit": UNIT,
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 1),
+        "step": (f"one bounded sample of the layer: every non-SKIP mode's query blocks at full N for "
+                 f"up to ~{budget:.1f} s on {base['cores']} cores; ms_per_step is that sample's wall time"),
+        "ms_per_layer": round(layer_ms, 1), "extrapolated": True,
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1) Q/K/V, one head per mode)",
+        "config": config_dict(cfg, cb.density, parallelism_label(mgpu, world)),
+        "cpu_baseline": base,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -621,6 +757,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -9,8 +9,8 @@
  *
  *   reference (file:line)                              replaced by
  *   layout.py:135-158  block_grid(layout)              svd_grid_size / svd_grid_arrays
- *   patterns.py:334-339 frame_period(grid)             svd_frame_period
- *   patterns.py:377-417 build_mask(spec, grid)         svd_mask_build
+ *   patterns.py:176-181 frame_period(grid)             svd_frame_period
+ *   patterns.py:219-259 build_mask(spec, grid)         svd_mask_build
  *   attention.py:164-183 group_heads(assignment, grid) svd_plan_create + svd_plan_group_* accessors
  *   attention.py:186-212 fused_layer_attention(...)    svd_attn_fwd
  *   attention.py:57-98  sparse_attention(q,k,v,mask)   svd_plan_create_from_masks + svd_attn_fwd
@@ -53,7 +53,7 @@ typedef enum svd_status {
   SVD_ERR_INTERNAL = 7
 } svd_status;
 
-typedef enum svd_mode {         /* patterns.py:189-194 Mode */
+typedef enum svd_mode {         /* patterns.py:31-36 Mode */
   SVD_FULL = 0,
   SVD_SKIP = 1,
   SVD_DIAGONAL = 2,
@@ -69,10 +69,10 @@ typedef struct svd_layout {
   int64_t block_size;
 } svd_layout;
 
-/* patterns.py:208-233 PatternSpec.  period <= 0 encodes None (frame period);
+/* patterns.py:50-75 PatternSpec.  period <= 0 encodes None (frame period);
  * n_stripes < 0 encodes stripes=None (unresolved).  Stripes may be given in
  * any order with duplicates: they are normalised to sorted-unique exactly as
- * PatternSpec.__post_init__ does (patterns.py:232-233). */
+ * PatternSpec.__post_init__ does (patterns.py:74-75). */
 typedef struct svd_spec {
   int32_t mode;
   int32_t halfwidth;
@@ -115,10 +115,10 @@ int svd_grid_size(const svd_layout* layout, int64_t* n_tokens, int64_t* n_blocks
 /* bounds: nb+1 entries; has_text, mixed: nb bytes; frame_index: nb entries. */
 int svd_grid_arrays(const svd_layout* layout, int64_t* bounds, uint8_t* has_text,
                     uint8_t* mixed, int64_t* frame_index);
-/* patterns.py:334-339 frame_period (round-half-even, clamped to >= 1). */
+/* patterns.py:176-181 frame_period (round-half-even, clamped to >= 1). */
 int svd_frame_period(const svd_layout* layout, int64_t* period);
 
-/* ---- patterns.py:377-417 build_mask ------------------------------------ */
+/* ---- patterns.py:219-259 build_mask ------------------------------------ */
 /* active: nb*nb bytes (row-major, 1 = active).  For SKIP *is_skip = 1 and
  * active is left untouched (the reference returns active=None). */
 int svd_mask_build(const svd_layout* layout, const svd_spec* spec, uint8_t* active,
@@ -141,7 +141,7 @@ int svd_plan_group_heads(const svd_plan* plan, int32_t g, int32_t* heads, int32_
 /* Block mask of group g (nb*nb bytes); SKIP groups return SVD_ERR_CONFIG. */
 int svd_plan_group_mask(const svd_plan* plan, int32_t g, uint8_t* active);
 /* CSR of group g's active key blocks, ascending per row
- * (patterns.py:363-366 active_key_blocks).  row_ptr: nb+1; col_idx: nnz. */
+ * (patterns.py:205-208 active_key_blocks).  row_ptr: nb+1; col_idx: nnz. */
 int svd_plan_group_nnz(const svd_plan* plan, int32_t g, int64_t* nnz);
 int svd_plan_group_csr(const svd_plan* plan, int32_t g, int64_t* row_ptr, int64_t* col_idx);
 /* The plan restricted to the listed heads, in that order (head i of the
@@ -196,6 +196,54 @@ int svd_attn_fwd_ex(const svd_plan* plan, const void* q, const void* k, const vo
                     const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
                     int32_t dtype, const int32_t* o_head_map, void* stream);
 
+/* As svd_attn_fwd_ex, with attention.py:98 require_finite fused into the
+ * epilogue: when any output row holds a non-finite value the kernel ORs 1
+ * into *nonfinite (device int32 the caller zeroes; NULL = no check).  The
+ * shim reads it back and raises ShapeError, as the reference does. */
+int svd_attn_fwd_v2(const svd_plan* plan, const void* q, const void* k, const void* v, void* o,
+                    const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                    const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                    int32_t dtype, const int32_t* o_head_map, int32_t* nonfinite, void* stream);
+
+/* The general form of the launch: every option of the operator in one
+ * struct (zero-initialise, then set what you need).
+ *   q, k, v, o, *_strides, batch, head_dim, tensor_dim, dtype: as svd_attn_fwd.
+ *   in_heads     heads of the q/k/v tensors (0 = the plan's heads).
+ *   in_head_map  device int32[plan heads]: plan head h reads q/k/v head
+ *                in_head_map[h] (NULL = identity) — e.g. the search's
+ *                candidate plan, whose heads are (candidate, head) pairs
+ *                over one set of q/k/v (search.py:334-372).
+ *   o_head_map   device int32[plan heads]: plan head h writes o head
+ *                o_head_map[h] (NULL = identity).
+ *   nonfinite    as svd_attn_fwd_v2 (NULL = no check).
+ *   row_stats    device float [batch * stats_heads][ceil(N / 128)][2][128]:
+ *                for every row of plan heads < stats_heads the softmax
+ *                statistics (-m, 1/l) in the log2 domain (m the row max of
+ *                s / sqrt(head_dim) * log2(e), l the sum of 2^(s' - m)), the
+ *                row-statistics pass of block_key_mass (NULL = none).  Rows
+ *                past N are written as (-inf, 0) where an item covers them. */
+typedef struct svd_fwd_args {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  int64_t q_strides[4];
+  int64_t k_strides[4];
+  int64_t v_strides[4];
+  int64_t o_strides[4];
+  int32_t batch;
+  int32_t head_dim;
+  int32_t tensor_dim;
+  int32_t dtype;
+  int32_t in_heads;
+  int32_t stats_heads;
+  const int32_t* in_head_map;
+  const int32_t* o_head_map;
+  int32_t* nonfinite;
+  float* row_stats;
+} svd_fwd_args;
+int svd_attn_fwd_args(const svd_plan* plan, const svd_fwd_args* args, void* stream);
+
 /* Fused compute + reassembly for multi-GPU: as svd_attn_fwd, but every
  * output row the plan (typically a svd_plan_shard view) produces is stored
  * into all n_peers O buffers — this rank's and its peers' [B, H, N,
@@ -215,6 +263,19 @@ int svd_attn_fwd_peers(const svd_plan* plan, const void* q, const void* k, const
 int svd_ipc_export(const void* ptr, uint8_t* handle64, int64_t* offset);
 int svd_ipc_import(const uint8_t* handle64, int64_t offset, void** ptr);
 int svd_ipc_close(void* ptr, int64_t offset);
+
+/* Stream-ordered barrier between the ranks of svd_attn_fwd_peers, over peer
+ * memory (no host synchronisation): flags[r] is rank r's int32[n_peers]
+ * flag array mapped into this process (flags[rank] = this rank's own).  The
+ * kernel stores `epoch` into slot `rank` of every rank's array (release,
+ * system scope) and waits until every slot of its own array reaches `epoch`
+ * (acquire).  Enqueued after the shard kernel, it completes once every
+ * rank's rows of that step are in every O.  Epochs increase by one per step
+ * (wrap-around safe).  A wait longer than timeout_s (<= 0: 30 s) stores 1 into
+ * *timed_out (device int32, may be NULL) and returns, so a dead peer cannot
+ * hang the GPU. */
+int svd_peer_barrier(int32_t* const* flags, int32_t n_peers, int32_t rank, int32_t epoch,
+                     int32_t* timed_out, double timeout_s, void* stream);
 
 /* Per-head sum of squared differences in fp64 (numerics.py:114-121 mse, the
  * search's reconstruction error, search.py:65-79): out[h] += sum over
@@ -237,6 +298,19 @@ int svd_block_key_mass(const void* q, const void* k, const int64_t* q_strides,
                        const int64_t* k_strides, int32_t batch, int32_t heads, int64_t n_tokens,
                        int32_t head_dim, int32_t tensor_dim, int32_t block_size, int32_t dtype,
                        void* workspace, int64_t workspace_bytes, double* mass, void* stream);
+
+/* block_key_mass's key-sum pass alone, given the row statistics a forward
+ * launch already produced (svd_fwd_args.row_stats of an all-FULL plan over
+ * the same q, k): the search's first evaluation of a layer gets the FULL
+ * candidate and the stripe calibration from one attention pass plus this
+ * key-sum pass.  row_stats: [batch * heads][ceil(N / 128)][2][128];
+ * workspace as svd_block_key_mass (its row-statistics part is unused). */
+int svd_block_key_mass_from_stats(const void* q, const void* k, const int64_t* q_strides,
+                                  const int64_t* k_strides, int32_t batch, int32_t heads,
+                                  int64_t n_tokens, int32_t head_dim, int32_t tensor_dim,
+                                  int32_t block_size, int32_t dtype, const float* row_stats,
+                                  void* workspace, int64_t workspace_bytes, double* mass,
+                                  void* stream);
 
 /* Scatter a gathered [world * max_rows, d] buffer of packed shard rows back
  * into O [B=1, H, N, d] (the multi-GPU reassembly after the NCCL all-gather). */

@@ -100,13 +100,51 @@ def block_grid(text: int, frames: int, tpf: int, block: int = 64) -> Grid:
 
 
 def frame_period(grid: Grid) -> int:
-    """patterns.py:334-339: max(1, round(tpf / block)), Python round = half-even."""
+    """patterns.py:176-181: max(1, round(tpf / block)), Python round = half-even."""
     return max(1, round(grid.tokens_per_frame / grid.block_size))
+
+
+# ------------------------------------------------------------------ specs
+class Spec(NamedTuple):
+    """PatternSpec's fields and defaults (patterns.py:50-66); enough for
+    build_mask / group_heads here.  Stripes are kept sorted and unique like
+    PatternSpec.__post_init__ (patterns.py:67-75)."""
+
+    mode: int
+    halfwidth: int = 1
+    period: int | None = None
+    md_halfwidth: int = 0
+    stripe_count: int = 2
+    stripes: tuple | None = None
+    include_diagonal: bool = True
+
+
+def full_spec() -> Spec:  # patterns.py:106-107
+    return Spec(FULL)
+
+
+def skip_spec() -> Spec:  # patterns.py:110-111
+    return Spec(SKIP)
+
+
+def diagonal_spec(halfwidth: int = 1) -> Spec:  # patterns.py:114-115
+    return Spec(DIAGONAL, halfwidth=halfwidth)
+
+
+def multi_diagonal_spec(period: int | None = None, md_halfwidth: int = 0) -> Spec:  # patterns.py:118-119
+    return Spec(MULTI_DIAGONAL, period=period, md_halfwidth=md_halfwidth)
+
+
+def vertical_stripe_spec(stripe_count: int = 2, stripes=None, include_diagonal: bool = True) -> Spec:
+    """patterns.py:122-132."""
+    return Spec(VERTICAL_STRIPE, stripe_count=stripe_count,
+                stripes=None if stripes is None else tuple(sorted(set(int(s) for s in stripes))),
+                include_diagonal=include_diagonal)
 
 
 # ------------------------------------------------------------------ masks
 def spec_key(spec) -> tuple:
-    """PatternSpec equality key (all dataclass fields, patterns.py:208-233)."""
+    """PatternSpec equality key (all dataclass fields, patterns.py:50-75)."""
     stripes = None if spec.stripes is None else tuple(sorted(set(int(s) for s in spec.stripes)))
     return (int(spec.mode), int(spec.halfwidth), spec.period, int(spec.md_halfwidth),
             int(spec.stripe_count), stripes, bool(spec.include_diagonal))
@@ -119,7 +157,7 @@ class OracleError(Exception):
 
 
 def build_mask(spec, grid: Grid):
-    """patterns.py:377-417.  Returns None for SKIP, else bool [nb, nb]."""
+    """patterns.py:219-259.  Returns None for SKIP, else bool [nb, nb]."""
     nb = grid.n_blocks
     mode = int(spec.mode)
     if mode == SKIP:
@@ -153,12 +191,12 @@ def build_mask(spec, grid: Grid):
 
 
 def active_key_blocks(active: np.ndarray, qb: int) -> np.ndarray:
-    """patterns.py:363-366."""
+    """patterns.py:205-208."""
     return np.flatnonzero(active[qb])
 
 
 def token_mask(active: np.ndarray, grid: Grid) -> np.ndarray:
-    """patterns.py:368-374."""
+    """patterns.py:210-216."""
     sizes = np.diff(grid.bounds)
     return np.repeat(np.repeat(active, sizes, axis=0), sizes, axis=1)
 
@@ -242,6 +280,31 @@ def sparse_attention_rows(q, k, v, active, bounds, qblocks) -> np.ndarray:
             acc = acc * alpha[..., None] + np.matmul(p, v[:, :, c0:c1].astype(np.float64))
             m = m_new
         outs.append((acc / l[..., None]).astype(np.float32))
+    return np.concatenate(outs, axis=2)
+
+
+def attention_rows(q, k, v, active, bounds, qblocks) -> np.ndarray:
+    """Output rows of the listed query blocks in one shot per block: the
+    softmax over the block's active key tokens (ascending, as
+    active_key_blocks lists them) in fp64 — the quantity attention.py:57-98's
+    streaming recurrence computes (it differs only by fp64 rounding, the
+    reference's own dense oracle tests/conftest.py:49-58 makes the same
+    comparison).  q, k, v: [B, H, N, d]; returns [B, H, sum rows, d] fp32."""
+    B, H, N, d = q.shape
+    scale = 1.0 / np.sqrt(d)
+    sizes = np.diff(bounds)
+    outs = []
+    for qb in qblocks:
+        r0, r1 = int(bounds[qb]), int(bounds[qb + 1])
+        kbs = np.flatnonzero(active[qb])
+        cols = np.concatenate([np.arange(bounds[c], bounds[c] + sizes[c]) for c in kbs])
+        q64 = np.asarray(q[:, :, r0:r1], dtype=np.float64)
+        k64 = np.asarray(k[:, :, cols], dtype=np.float64)
+        v64 = np.asarray(v[:, :, cols], dtype=np.float64)
+        s = np.matmul(q64, k64.swapaxes(-1, -2)) * scale
+        s -= s.max(axis=-1, keepdims=True)
+        p = np.exp(s)
+        outs.append((np.matmul(p, v64) / p.sum(axis=-1, keepdims=True)).astype(np.float32))
     return np.concatenate(outs, axis=2)
 
 

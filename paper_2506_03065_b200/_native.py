@@ -77,6 +77,20 @@ class SvdPlanInfo(ctypes.Structure):
     ]
 
 
+class SvdFwdArgs(ctypes.Structure):
+    """include/svdit_b200.h svd_fwd_args."""
+
+    _fields_ = [
+        ("q", c_void_p), ("k", c_void_p), ("v", c_void_p), ("o", c_void_p),
+        ("q_strides", c_int64 * 4), ("k_strides", c_int64 * 4), ("v_strides", c_int64 * 4),
+        ("o_strides", c_int64 * 4),
+        ("batch", c_int32), ("head_dim", c_int32), ("tensor_dim", c_int32), ("dtype", c_int32),
+        ("in_heads", c_int32), ("stats_heads", c_int32),
+        ("in_head_map", c_void_p), ("o_head_map", c_void_p), ("nonfinite", c_void_p),
+        ("row_stats", c_void_p),
+    ]
+
+
 # every exported symbol with its signature (restype, argtypes)
 SIGNATURES = {
     "svd_last_error": (c_char_p, []),
@@ -114,12 +128,25 @@ SIGNATURES = {
          POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
          c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p],
     ),
+    "svd_attn_fwd_v2": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+         POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
+         c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p],
+    ),
+    "svd_attn_fwd_args": (c_int, [c_void_p, POINTER(SvdFwdArgs), c_void_p]),
+    "svd_block_key_mass_from_stats": (
+        c_int,
+        [c_void_p, c_void_p, POINTER(c_int64), POINTER(c_int64), c_int32, c_int32, c_int64, c_int32,
+         c_int32, c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p],
+    ),
     "svd_attn_fwd_peers": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
          POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
          c_int32, c_int32, c_int32, c_int32, c_void_p],
     ),
+    "svd_peer_barrier": (c_int, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_double, c_void_p]),
     "svd_ipc_export": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "svd_ipc_import": (c_int, [c_void_p, c_int64, POINTER(c_void_p)]),
     "svd_ipc_close": (c_int, [c_void_p, c_int64]),

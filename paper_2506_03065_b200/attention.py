@@ -192,7 +192,8 @@ class LayerPlan:
         return heads[: n.value], toks[: n.value]
 
     # -- execution
-    def forward(self, q, k, v, out, head_dim: int | None = None, stream=None, o_head_map=None) -> None:
+    def forward(self, q, k, v, out, head_dim: int | None = None, stream=None, o_head_map=None,
+                nonfinite=None, in_head_map=None, row_stats=None, stats_heads: int = 0) -> None:
         """Launch the fused layer kernel on prepared bf16 CUDA tensors.
 
         q, k, v: [B, H, N, D] views with unit stride on D (D = 64 or 128);
@@ -200,25 +201,41 @@ class LayerPlan:
         No host synchronisation; runs on `stream` (default: current stream).
         o_head_map: optional device int32 [H] tensor — plan head h writes head
         o_head_map[h] of `out` (a head-subset plan into a full-layer O).
+        nonfinite: optional device int32 [1] tensor the epilogue ORs 1 into
+        when an output row is non-finite (attention.py:98 require_finite).
+        in_head_map: optional device int32 [plan heads] — plan head h reads
+        q/k/v head in_head_map[h] (q/k/v may then hold fewer heads).
+        row_stats / stats_heads: optional float32 device tensor
+        [B * stats_heads, ceil(N / 128), 2, 128] receiving (-m, 1/l) of every
+        row of plan heads < stats_heads (block_key_mass's row statistics).
         """
         import torch
 
         d_t = q.shape[-1]
         hd = int(head_dim if head_dim is not None else d_t)
-        if stream is None:
-            stream = torch.cuda.current_stream(q.device)
-        st = [nat.i64x4(t.stride()) for t in (q, k, v)]
-        if self.sharded:
-            ost = nat.i64x4((0, 0, out.stride(0), out.stride(1)))
-            batch = 1
-        else:
-            ost = nat.i64x4(out.stride())
-            batch = q.shape[0]
-        hmap = nat.c_void_p(o_head_map.data_ptr()) if o_head_map is not None else None
-        nat.check(nat.lib().svd_attn_fwd_ex(
-            self._handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
-            nat.c_void_p(v.data_ptr()), nat.c_void_p(out.data_ptr()), st[0], st[1], st[2], ost,
-            int(batch), hd, int(d_t), 0, hmap, nat.c_void_p(stream.cuda_stream)))
+        with torch.cuda.device(q.device):  # plan tables / tensor maps on q's device
+            if stream is None:
+                stream = torch.cuda.current_stream(q.device)
+            a = nat.SvdFwdArgs()
+            a.q, a.k, a.v, a.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
+            a.q_strides[:] = list(q.stride())
+            a.k_strides[:] = list(k.stride())
+            a.v_strides[:] = list(v.stride())
+            if self.sharded:
+                a.o_strides[:] = [0, 0, out.stride(0), out.stride(1)]
+                a.batch = 1
+            else:
+                a.o_strides[:] = list(out.stride())
+                a.batch = q.shape[0]
+            a.head_dim, a.tensor_dim, a.dtype = hd, int(d_t), 0
+            a.in_heads = int(q.shape[1]) if in_head_map is not None else 0
+            a.in_head_map = in_head_map.data_ptr() if in_head_map is not None else None
+            a.o_head_map = o_head_map.data_ptr() if o_head_map is not None else None
+            a.nonfinite = nonfinite.data_ptr() if nonfinite is not None else None
+            a.row_stats = row_stats.data_ptr() if row_stats is not None else None
+            a.stats_heads = int(stats_heads) if row_stats is not None else 0
+            nat.check(nat.lib().svd_attn_fwd_args(self._handle, nat.ctypes.byref(a),
+                                                  nat.c_void_p(stream.cuda_stream)))
 
 
 def _device_sm_count() -> int:
@@ -323,6 +340,9 @@ PCIE_BYTES_PER_S = float(__import__("os").environ.get("SVD_PCIE_GBPS", "50")) * 
 HOST_ZERO_COPY = __import__("os").environ.get("SVD_HOST_ZERO_COPY", "0") == "1"
 # consecutive chunk kernels on two alternating streams (SVD_HOST_OVERLAP=0: one)
 HOST_OVERLAP = __import__("os").environ.get("SVD_HOST_OVERLAP", "1") == "1"
+# attention.py:98 require_finite on every call (a device flag set by the
+# kernel epilogue, read back after the launch); SVD_REQUIRE_FINITE=0 skips it
+REQUIRE_FINITE = __import__("os").environ.get("SVD_REQUIRE_FINITE", "1") != "0"
 # Per-SM kernel time per KV step of a work item (two 128-row tiles x 128
 # keys), measured on B200 at power-capped clocks: HunyuanVideo 40.5 ms x 148
 # SMs / 2.89 M steps (d=128), CogVideoX 35.7 ms x 148 / 3.48 M (d=64); plus a
@@ -579,8 +599,9 @@ def _run_host(plan: LayerPlan, q, k, v, out=None, numpy_out: bool = False):
         # host O through a per-chunk head map (no copy-out stage to drain)
         zero_copy = (HOST_ZERO_COPY and D == d and direct_out and out_host.is_contiguous())
         streams = (compute, st.s_comp) if HOST_OVERLAP else (compute,)
-        st.s_comp.wait_stream(compute)  # the caller's prior work on its stream
-        finite = []
+        # attention.py:98 require_finite, fused into the kernel epilogue
+        flag = torch.zeros(1, dtype=torch.int32, device=dev) if REQUIRE_FINITE else None
+        st.s_comp.wait_stream(compute)  # the caller's prior work on its stream (and the flag's zero-fill)
         copied = []   # per chunk: D2H done event
         drained = 0   # chunks whose results are in out_host
 
@@ -615,14 +636,11 @@ def _run_host(plan: LayerPlan, q, k, v, out=None, numpy_out: bool = False):
             sub = plan.heads_subplan(tuple(order[s0:s1]))
             if zero_copy:
                 sub.forward(qc, kc, vc, out_host, head_dim=d, stream=cs,
-                            o_head_map=st.head_map(order, s0, s1))
+                            o_head_map=st.head_map(order, s0, s1), nonfinite=flag)
                 continue
-            sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=cs)
+            sub.forward(qc, kc, vc, st.o[:, s0:s1], head_dim=d, stream=cs, nonfinite=flag)
             computed = torch.cuda.Event()
             computed.record(cs)
-            if numpy_out:  # attention.py:98 require_finite, reduced on the device
-                with torch.cuda.stream(cs):
-                    finite.append(torch.isfinite(st.o[:, s0:s1, :, :d]).all())
             with torch.cuda.stream(s_out):
                 s_out.wait_event(computed)
                 for slot in range(s0, s1):
@@ -643,7 +661,7 @@ def _run_host(plan: LayerPlan, q, k, v, out=None, numpy_out: bool = False):
             s_out.synchronize()  # a host result must be readable on return
         else:
             drain(chunks, block=True)
-        if numpy_out and not bool(torch.stack(finite).all()):
+        if flag is not None and int(flag.item()) != 0:
             raise ShapeError("non-finite values in attention output")
     return res if numpy_out else out_host
 
@@ -683,25 +701,32 @@ def _run(plan: LayerPlan, q, k, v, out=None):
         return _run_host(plan, *ts, numpy_out=True)
     (qt, kt, vt), was_numpy, dev = _to_device((q, k, v))
     dt = qt.shape[-1]
+    # attention.py:98 require_finite: the epilogue flags non-finite rows; reading
+    # the flag back synchronises (SVD_REQUIRE_FINITE=0 keeps the call async)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if REQUIRE_FINITE else None
     if out is not None:
         _check_out(out, (B, H, N, d), "cuda")
         if dt == d and all((st * 2) % 16 == 0 for st in out.stride()[:-1]) and out.data_ptr() % 16 == 0:
-            plan.forward(qt, kt, vt, out, head_dim=d)
+            plan.forward(qt, kt, vt, out, head_dim=d, nonfinite=flag)
         else:
             tmp = torch.empty((B, H, N, dt), dtype=torch.bfloat16, device=dev)
-            plan.forward(qt, kt, vt, tmp, head_dim=d)
+            plan.forward(qt, kt, vt, tmp, head_dim=d, nonfinite=flag)
             out.copy_(tmp[..., :d])
+        _require_finite(flag)
         return out
     out = torch.empty((B, H, N, dt), dtype=torch.bfloat16, device=dev)
-    plan.forward(qt, kt, vt, out, head_dim=d)
+    plan.forward(qt, kt, vt, out, head_dim=d, nonfinite=flag)
     if dt != d:
         out = out[..., :d]
+    _require_finite(flag)
     if was_numpy:
-        res = out.float().cpu().numpy()
-        if not np.isfinite(res).all():
-            raise ShapeError("non-finite values in attention output")
-        return res
+        return out.float().cpu().numpy()
     return out
+
+
+def _require_finite(flag) -> None:
+    if flag is not None and int(flag.item()) != 0:
+        raise ShapeError("non-finite values in attention output")
 
 
 # ---------------------------------------------------------------- reference API
@@ -745,8 +770,11 @@ def group_heads(assignment, grid: BlockGrid) -> list[HeadGroup]:
         spec = assignment[heads[0]]
         mask = None
         if int(spec.mode) not in (Mode.FULL, Mode.SKIP):
-            mask = BlockMask(grid=grid, active=plan.group_mask(g))
+            active = plan.group_mask(g)
+            active.setflags(write=False)  # shared by every caller: immutable like the plan
+            mask = BlockMask(grid=grid, active=active)
         groups.append(HeadGroup(spec=spec, heads=heads, mask=mask, plan=plan))
+    plan.__dict__["_groups"] = tuple(groups)
     _GROUP_CACHE[key] = groups
     while len(_GROUP_CACHE) > _PLAN_CACHE_MAX:
         _GROUP_CACHE.popitem(last=False)
@@ -758,10 +786,14 @@ def _plan_for_groups(groups, H: int, N: int) -> LayerPlan:
     plans = {id(getattr(g, "plan", None)) for g in groups}
     first = getattr(groups[0], "plan", None)
     if len(plans) == 1 and first is not None and first.n_heads == H:
-        # the groups came from one group_heads() call: check they are that plan's
-        info = first.info
-        if info.n_groups == len(groups) and all(
-                first.group_heads(i)[0] == g.heads for i, g in enumerate(groups)):
+        # the groups came from one group_heads() call: reuse its plan only if
+        # every group is still what that call produced (same heads, spec and
+        # the very mask object — dataclasses.replace(g, mask=...) keeps
+        # g.plan, so an edited group must be lowered from its own mask)
+        made = first.__dict__.get("_groups", ())
+        if len(made) == len(groups) and all(
+                g.heads == m.heads and g.spec == m.spec and g.mask is m.mask
+                for g, m in zip(groups, made)):
             return first
     # hand-built groups: lower their masks explicitly
     layout = None
@@ -804,6 +836,33 @@ def fused_layer_attention(q, k, v, groups, out=None):
 
 
 _MASK_PLANS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_MASK_CONTENT_PLANS: "OrderedDict[tuple, LayerPlan]" = OrderedDict()
+
+
+def _mask_plan(mask: BlockMask, H: int) -> LayerPlan:
+    """Plan for one mask over H heads.  Read-only masks (the ones group_heads /
+    build_mask hand out) are cached by identity; a writable mask may be edited
+    in place between calls, so it is keyed by its content."""
+    active = np.asarray(mask.active)
+    if not active.flags.writeable:
+        per_mask = _MASK_PLANS.setdefault(mask, {})
+        plan = per_mask.get(H)
+        if plan is None:
+            plan = per_mask[H] = LayerPlan.from_masks(mask.grid.layout, [active], np.zeros(H, dtype=np.int32))
+        return plan
+    import hashlib
+
+    key = (mask.grid.layout, H, active.shape,
+           hashlib.blake2b(np.packbits(active.astype(bool, copy=False)).tobytes(), digest_size=16).digest())
+    plan = _MASK_CONTENT_PLANS.get(key)
+    if plan is None:
+        plan = LayerPlan.from_masks(mask.grid.layout, [active], np.zeros(H, dtype=np.int32))
+        _MASK_CONTENT_PLANS[key] = plan
+        while len(_MASK_CONTENT_PLANS) > _PLAN_CACHE_MAX:
+            _MASK_CONTENT_PLANS.popitem(last=False)
+    else:
+        _MASK_CONTENT_PLANS.move_to_end(key)
+    return plan
 
 
 def sparse_attention(q, k, v, mask: BlockMask):
@@ -815,12 +874,7 @@ def sparse_attention(q, k, v, mask: BlockMask):
         raise DegenerateRowError("skip mask defines no softmax; use skip_attention")
     if not np.asarray(mask.active).any(axis=1).all():
         raise DegenerateRowError("mask has a query row with no active key blocks")
-    per_mask = _MASK_PLANS.setdefault(mask, {})
-    plan = per_mask.get(H)
-    if plan is None:
-        plan = LayerPlan.from_masks(mask.grid.layout, [mask.active], np.zeros(H, dtype=np.int32))
-        per_mask[H] = plan
-    return _run(plan, q, k, v)
+    return _run(_mask_plan(mask, H), q, k, v)
 
 
 def full_mask_attention(q, k, v, grid: BlockGrid):

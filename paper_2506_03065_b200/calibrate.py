@@ -36,10 +36,11 @@ def head_sqdiff(a, b=None):
 
     B, H, N, d = a.shape
     out = torch.zeros(H, dtype=torch.float64, device=a.device)
-    nat.check(nat.lib().svd_head_sqdiff(
-        nat.c_void_p(a.data_ptr()), nat.c_void_p(b.data_ptr()) if b is not None else None,
-        nat.i64x4(a.stride()), nat.i64x4(b.stride() if b is not None else a.stride()), B, H, N, d,
-        nat.c_void_p(out.data_ptr()), nat.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)))
+    with torch.cuda.device(a.device):
+        nat.check(nat.lib().svd_head_sqdiff(
+            nat.c_void_p(a.data_ptr()), nat.c_void_p(b.data_ptr()) if b is not None else None,
+            nat.i64x4(a.stride()), nat.i64x4(b.stride() if b is not None else a.stride()), B, H, N, d,
+            nat.c_void_p(out.data_ptr()), nat.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)))
     return out
 
 
@@ -65,16 +66,41 @@ def block_key_mass(q, k, grid: BlockGrid):
     nb = grid.n_blocks
     lib = nat.lib()
     ws_bytes = int(lib.svd_key_mass_workspace(B, H, N))
-    stream = torch.cuda.current_stream(dev)
-    ws = _workspace(dev, stream, ws_bytes)
-    mass = torch.empty(B, H, nb, dtype=torch.float64, device=dev)
-    nat.check(lib.svd_block_key_mass(
-        nat.c_void_p(qt.data_ptr()), nat.c_void_p(kt.data_ptr()), nat.i64x4(qt.stride()),
-        nat.i64x4(kt.stride()), B, H, N, d, D, int(grid.layout.block_size), 0,
-        nat.c_void_p(ws.data_ptr()), ws_bytes, nat.c_void_p(mass.data_ptr()),
-        nat.c_void_p(stream.cuda_stream)))
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = _workspace(dev, stream, ws_bytes)
+        mass = torch.empty(B, H, nb, dtype=torch.float64, device=dev)
+        nat.check(lib.svd_block_key_mass(
+            nat.c_void_p(qt.data_ptr()), nat.c_void_p(kt.data_ptr()), nat.i64x4(qt.stride()),
+            nat.i64x4(kt.stride()), B, H, N, d, D, int(grid.layout.block_size), 0,
+            nat.c_void_p(ws.data_ptr()), ws_bytes, nat.c_void_p(mass.data_ptr()),
+            nat.c_void_p(stream.cuda_stream)))
     if was_numpy:
         return mass.cpu().numpy()
+    return mass
+
+
+def block_key_mass_from_stats(q, k, grid: BlockGrid, row_stats, head_dim: int | None = None):
+    """block_key_mass (attention.py:108-146) for bf16 CUDA q, k [B, H, N, D]
+    whose row statistics (-m, 1/l) a forward launch already wrote
+    (LayerPlan.forward(row_stats=...) on an all-FULL plan): only the key-sum
+    pass and the block sum run.  head_dim: the true d when q/k are zero-padded
+    to D.  Returns a float64 CUDA tensor [B, H, nb]."""
+    import torch
+
+    B, H, N, D = q.shape
+    lib = nat.lib()
+    ws_bytes = int(lib.svd_key_mass_workspace(B, H, N))
+    dev = q.device
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = _workspace(dev, stream, ws_bytes)
+        mass = torch.empty(B, H, grid.n_blocks, dtype=torch.float64, device=dev)
+        nat.check(lib.svd_block_key_mass_from_stats(
+            nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()), nat.i64x4(q.stride()),
+            nat.i64x4(k.stride()), B, H, N, int(head_dim or D), D, int(grid.layout.block_size), 0,
+            nat.c_void_p(row_stats.data_ptr()), nat.c_void_p(ws.data_ptr()), ws_bytes,
+            nat.c_void_p(mass.data_ptr()), nat.c_void_p(stream.cuda_stream)))
     return mass
 
 
@@ -110,7 +136,24 @@ class LayerEvaluation:
 
 
 class CandidateEvaluator:
-    """One layer's candidate evaluation (search.py:334-372) on the GPU."""
+    """One layer's candidate evaluation (search.py:334-372) on the GPU.
+
+    The four candidates run as ONE launch of the fused layer kernel: its
+    plan has 4H heads — (FULL, diagonal, multi-diagonal, stripe) x H, the
+    stripe heads with their own columns — all reading the layer's single
+    q/k/v through an input head map, heaviest work items first, so the
+    sparse candidates' items fill the FULL items' tail instead of paying three
+    more launches.  The FULL candidate's launch also writes every row's
+    softmax statistics (-m, 1/l), so the stripe calibration
+    (block_key_mass, attention.py:108-146) needs only its key-sum pass.
+
+    First evaluation of a layer (stripe columns unknown; the reference
+    freezes them there, search.py:338-346): launch 1 = FULL + diagonal +
+    multi-diagonal (+ row statistics), key-sum pass -> stripes, launch 2 =
+    the stripe candidates.  Every later evaluation (stripes given): one
+    launch.  The per-head fp64 MSE is svd_head_sqdiff; mode_loss /
+    select_mode are the unchanged reference plugin surface.
+    """
 
     def __init__(self, grid: BlockGrid, params: SearchParams | None = None, latency_model=None):
         """latency_model (a costmodel.B200LatencyModel): when given, the
@@ -128,6 +171,7 @@ class CandidateEvaluator:
         self._s_diag = build_mask(self._diag, grid).sparsity
         self._s_md = build_mask(self._md, grid).sparsity
         self._s_stripe: dict = {}
+        self._maps: dict = {}
 
     def stripe_sparsity(self, cols) -> float:
         from .patterns import build_mask
@@ -150,28 +194,59 @@ class CandidateEvaluator:
         m0 = mass[0].double().cpu().numpy() if _is_torch(mass) else mass[0]
         return {h: top_stripes(m0[i], self.params.patterns.stripe_count) for i, h in enumerate(heads)}
 
+    def _stripe_specs(self, stripes, H):
+        pp = self.params.patterns
+        return [pp.spec_for(Mode.VERTICAL_STRIPE, stripes[h]) for h in range(H)]
+
+    def _in_map(self, dev, H: int, copies: int):
+        import torch
+
+        key = (dev.index, H, copies)
+        if key not in self._maps:
+            self._maps[key] = torch.arange(H, dtype=torch.int32, device=dev).repeat(copies)
+        return self._maps[key]
+
+    def _launch(self, asg, qt, kt, vt, d, copies, row_stats=None):
+        """One launch of the candidate plan `asg` (copies x H heads over the
+        H heads of qt/kt/vt) -> [B, copies * H, N, D] bf16."""
+        import torch
+
+        B, H, N, D = qt.shape
+        out = torch.empty(B, copies * H, N, D, dtype=torch.bfloat16, device=qt.device)
+        plan = plan_for_assignment(asg, self.grid.layout)
+        in_map = self._in_map(qt.device, H, copies) if copies > 1 else None
+        plan.forward(qt, kt, vt, out, head_dim=d, in_head_map=in_map, row_stats=row_stats,
+                     stats_heads=H if row_stats is not None else 0)
+        return out
+
     def evaluate(self, q, k, v, stripes: dict | None = None) -> LayerEvaluation:
         import torch
 
         B, H, N, d = _check_qkv(q, k, v)
         (qt, kt, vt), _, dev = _to_device((q, k, v))
+        D = qt.shape[-1]
         stripes = dict(stripes or {})
         missing = [h for h in range(H) if h not in stripes]
+        fulls, diags, mds = [full_spec()] * H, [self._diag] * H, [self._md] * H
         if missing:
-            stripes.update(self.resolve_stripes(qt[..., :d], kt[..., :d], missing))
-        layout = self.grid.layout
-        pp = self.params.patterns
-        cands = {
-            "full": [full_spec()] * H,
-            "diag": [self._diag] * H,
-            "md": [self._md] * H,
-            "stripe": [pp.spec_for(Mode.VERTICAL_STRIPE, stripes[h]) for h in range(H)],
-        }
-        outs = {}
-        for name, asg in cands.items():
-            o = torch.empty_like(qt)
-            plan_for_assignment(asg, layout).forward(qt, kt, vt, o, head_dim=d)
-            outs[name] = o[..., :d] if o.shape[-1] != d else o
+            # launch 1: FULL + diagonal + multi-diagonal, FULL rows' statistics
+            T = (N + 127) // 128
+            stats = torch.empty(B * H, T, 2, 128, dtype=torch.float32, device=dev)
+            stats[:, :, 0].fill_(float("-inf"))
+            stats[:, :, 1].zero_()
+            o3 = self._launch(fulls + diags + mds, qt, kt, vt, d, 3, row_stats=stats)
+            mass = block_key_mass_from_stats(qt, kt, self.grid, stats, head_dim=d)
+            m0 = mass[0].double().cpu().numpy()
+            for h in missing:
+                stripes[h] = top_stripes(m0[h], self.params.patterns.stripe_count)
+            o_st = self._launch(self._stripe_specs(stripes, H), qt, kt, vt, d, 1)
+            outs = {"full": o3[:, :H], "diag": o3[:, H:2 * H], "md": o3[:, 2 * H:], "stripe": o_st}
+        else:
+            o4 = self._launch(fulls + diags + mds + self._stripe_specs(stripes, H), qt, kt, vt, d, 4)
+            outs = {"full": o4[:, :H], "diag": o4[:, H:2 * H], "md": o4[:, 2 * H:3 * H],
+                    "stripe": o4[:, 3 * H:]}
+        if D != d:
+            outs = {c: o[..., :d] for c, o in outs.items()}
         full = outs["full"]
         denom = float(B * N * d)
         sq = torch.stack([head_sqdiff(full), head_sqdiff(outs["diag"], full),
@@ -180,6 +255,8 @@ class CandidateEvaluator:
         sparsities = np.array([[1.0, self._s_diag, self._s_md, self.stripe_sparsity(stripes[h])]
                                for h in range(H)])
         if self.latency_model is not None:
+            layout = self.grid.layout
+
             # per-head issued-tile counts of each candidate's schedule
             def head_tiles(asg):
                 items, _ = plan_for_assignment(asg, layout).schedule()
@@ -187,8 +264,8 @@ class CandidateEvaluator:
                 np.add.at(t, items[:, 0], 2 * np.maximum(items[:, 3], 0))
                 return t
 
-            t_full = head_tiles(cands["full"])
-            t_c = [head_tiles(cands[c]) for c in ("diag", "md", "stripe")]
+            t_full = head_tiles(fulls)
+            t_c = [head_tiles(c) for c in (diags, mds, self._stripe_specs(stripes, H))]
             lm = self.latency_model
             for h in range(H):
                 for ci, tc in enumerate(t_c):
@@ -209,5 +286,5 @@ class CandidateEvaluator:
                                stripes=stripes, selected=sel)
 
 
-__all__ = ["block_key_mass", "head_sqdiff", "top_stripes", "CandidateEvaluator", "LayerEvaluation",
+__all__ = ["block_key_mass", "block_key_mass_from_stats", "head_sqdiff", "top_stripes", "CandidateEvaluator", "LayerEvaluation",
            "SPARSE_MODES"]

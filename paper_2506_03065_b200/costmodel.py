@@ -72,10 +72,17 @@ class B200LatencyModel:
 
     def effective_sparsity(self, computed_tiles: int, full_tiles: int, head_dim: int) -> float:
         """1 - t(pattern) / t(full) on the throughput term: the latency-weighted
-        sparsity that drops into mode_loss's sparsity slot (search.py:65-79)."""
-        t = self.predict_ms(computed_tiles, head_dim)
-        t_full = self.predict_ms(full_tiles, head_dim)
-        return min(1.0, max(0.0, 1.0 - t / t_full))
+        sparsity that drops into mode_loss's sparsity slot (search.py:65-79).
+        Per head: the whole-launch constant launch_ms is left out (it is paid
+        once per layer, not per head), and head_dim is the kernel's stored
+        width (64 or 128: smaller head dims run zero-padded)."""
+        d = 64 if int(head_dim) <= 64 else 128
+        per = self.ms_per_tile.get(d)
+        if per is None:
+            raise ConfigError(f"no latency fit for head_dim {head_dim}")
+        if full_tiles <= 0:
+            return 0.0
+        return min(1.0, max(0.0, 1.0 - (computed_tiles * per) / (full_tiles * per)))
 
     def save(self, path) -> None:
         Path(path).write_text(json.dumps({

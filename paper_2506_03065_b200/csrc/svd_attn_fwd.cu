@@ -135,7 +135,27 @@ struct FwdParams {
   int max_split_parts;
   // optional output head permutation: plan head h writes O head o_head_map[h]
   const int32_t* o_head_map;
+  // attention.py:98 require_finite: OR-ed with 1 when an output row is non-finite
+  int* nonfinite;
+  // optional input head permutation: plan head h reads Q/K/V head in_head_map[h]
+  const int32_t* in_head_map;
+  // optional per-row softmax statistics (-m, 1/l) of plan heads < stats_heads,
+  // in block_key_mass's pass-0 layout [B * stats_heads][n_tiles128][2][128]
+  float* row_stats;
+  int stats_heads;
+  int n_tiles128;
 };
+
+// (-m, 1/l) of one row into the key-mass row-statistics layout
+__device__ __forceinline__ void store_row_stats(const FwdParams& p, int b, int head, int tok, bool valid,
+                                                float m, float l) {
+  if (!p.row_stats || head >= p.stats_heads || tok < 0) return;
+  const int64_t bh = int64_t(b) * p.stats_heads + head;
+  float* sp = p.row_stats + (bh * p.n_tiles128 + (tok >> 7)) * 256;
+  const bool ok = valid && l > 0.f;
+  sp[tok & 127] = ok ? -m : -INFINITY;
+  sp[128 + (tok & 127)] = ok ? 1.0f / l : 0.f;
+}
 
 // Store one 16-byte chunk of an output row: to o + off, or to every peer.
 __device__ __forceinline__ void store_row16(const FwdParams& p, int64_t off, const uint4& val) {
@@ -314,8 +334,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // Register split: the producer / MMA warpgroup needs few registers, the two
   // softmax warpgroups hold a 128-wide fp32 row of S each.
+#ifndef SVD_REG_LOW
+#define SVD_REG_LOW 56
+#endif
+#ifndef SVD_REG_HIGH
+#define SVD_REG_HIGH 224
+#endif
   if (warp < 4) {
-    ptx::reg_dealloc<56>();
+    ptx::reg_dealloc<SVD_REG_LOW>();
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer
       if (lane == 0 && n_kv > 0) {
@@ -325,13 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t pol_q = ptx::policy_evict_first();
         const uint64_t pol_kv = ptx::policy_evict_last();
         const int first = itp->qseg[0];
+        const int in_head = p.in_head_map ? __ldg(p.in_head_map + head) : head;
         ptx::mbar_arrive_expect_tx(bar(C::kBarQ), 2 * C::kTileBytes);
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           int s0 = itp->qseg[2 * x], s1 = itp->qseg[2 * x + 1];
           s0 = s0 >= 0 ? s0 : first;
           s1 = s1 >= 0 ? s1 : first;
-          load_tile<D>(&tm_q, base + C::kOffQ + x * C::kTileBytes, bar(C::kBarQ), s0, s1, head, b,
+          load_tile<D>(&tm_q, base + C::kOffQ + x * C::kTileBytes, bar(C::kBarQ), s0, s1, in_head, b,
                        pol_q);
         }
         const KvEntry* kvp = p.kv + itp->kv_begin;
@@ -348,11 +375,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
           ptx::mbar_arrive_expect_tx(bar(C::kBarKF + ks), C::kTileBytes);
           load_tile<D>(&tm_k, base + C::kOffK + ks * C::kTileBytes, bar(C::kBarKF + ks), k0, k1,
-                       head, b, pol_kv);
+                       in_head, b, pol_kv);
           ptx::mbar_wait(bar(C::kBarVE + vs), ((j / C::kVSt) & 1) ^ 1);
           ptx::mbar_arrive_expect_tx(bar(C::kBarVF + vs), C::kTileBytes);
           load_tile<D>(&tm_v, base + C::kOffV + vs * C::kTileBytes, bar(C::kBarVF + vs), k0, k1,
-                       head, b, pol_kv);
+                       in_head, b, pol_kv);
         }
       }
       __syncwarp();
@@ -484,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }  // warp < 4
 
   // -------------------------------------------------------------- softmax / epilogue
-  ptx::reg_alloc<224>();
+  ptx::reg_alloc<SVD_REG_HIGH>();
   const int x = (warp - 4) >> 2;           // Q tile A (0) or B (1)
   const int wq = warp & 3;                 // TMEM lane quarter
   const int row = wq * 32 + lane;          // row of the 128-row tile
@@ -544,10 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         pv.y = ptx::ex2(xv.y);
       }
       pk[i] = ptx::pack_bf16(pv.x, pv.y);
-      if (!(SVD_SUM_AFTER_ST && D == 128)) {
-        if (SVD_SUM_ROUNDED) ptx::acc_bf16x2(acc[i & 3], pk[i]);
-        else acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
-      }
+      if (!SVD_SUM_ROUNDED) acc[i & 3] = ptx::fadd2(acc[i & 3], pv);
+      else if (!(SVD_SUM_AFTER_ST && D == 128)) ptx::acc_bf16x2(acc[i & 3], pk[i]);
     }
   };
   const uint32_t tp = tmem + lane_off + C::col_p(x);
@@ -618,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[16];
       exp_chunk(s, c, nm, pk, acc);
       ptx::tmem_st16(tp + c * 16, pk);
-      if (SVD_SUM_AFTER_ST && D == 128) {
+      if (SVD_SUM_ROUNDED && SVD_SUM_AFTER_ST && D == 128) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) ptx::acc_bf16x2(acc[i & 3], pk[i]);
       }
@@ -648,6 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t to = tmem + lane_off + C::col_o(x);
   if (itp->split_group < 0) {
     const float inv = l > 0.f ? 1.0f / l : 0.f;
+    float chk = l * 0.f;  // NaN once any accumulator (or l) is Inf / NaN
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       float ov[32];
@@ -656,6 +682,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) chk = fmaf(ov[i], 0.f, chk);
       if (row_valid) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -663,6 +691,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                       make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
       }
     }
+    if (p.nonfinite && row_valid && chk != 0.f) atomicOr(p.nonfinite, 1);
+    if (qseg >= 0) store_row_stats(p, b, head, tok_r, row_valid, m, l);
   } else {
     // split-KV part: publish the partial state (O relative to m, l), then the
     // part that finishes last merges all parts (flash-decoding style):
@@ -730,6 +760,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(acc[2 * i] * inv, acc[2 * i + 1] * inv);
+        float chk = L * 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) chk = fmaf(acc[i], 0.f, chk);
+        if (p.nonfinite && row_valid && chk != 0.f) atomicOr(p.nonfinite, 1);
         if (row_valid) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -737,12 +771,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                         make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
         }
       }
+      if (qseg >= 0) store_row_stats(p, b, head, tok_r, row_valid, M, L);
       if (threadIdx.x == 128) p.split_tickets[sg] = 0;  // ready for the next launch
     }
   }
   if (p.n_peers > 0) __threadfence_system();  // peer rows visible before the kernel retires
   ptx::tc_fence_before();
   named_bar_sync(1, 32 + 256);
+}
+
+// Stream-ordered barrier over peer memory (multi-GPU step boundary without a
+// host sync): thread r publishes `epoch` into slot `rank` of rank r's flag
+// array (release, system scope), then thread r waits until slot r of this
+// rank's own array reaches `epoch` (acquire).  Stream order puts it after the
+// shard kernel, whose peer stores are fenced system-wide.  A wait longer than
+// timeout_ns sets *timed_out and gives up (a dead peer must not hang the GPU).
+struct PeerFlags {
+  int32_t* f[kMaxPeers];
+};
+__global__ void svd_peer_barrier_kernel(PeerFlags flags, int n, int rank, int32_t epoch,
+                                        int32_t* timed_out, uint64_t timeout_ns) {
+  const int r = threadIdx.x;
+  if (r >= n) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(flags.f[r] + rank), "r"(epoch) : "memory");
+  const int32_t* mine = flags.f[rank] + r;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    int32_t v;
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+    if (int32_t(uint32_t(v) - uint32_t(epoch)) >= 0) break;  // wrap-around safe
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      if (timed_out) atomicExch(timed_out, 1);
+      break;
+    }
+    __nanosleep(200);
+  }
 }
 
 // Multi-GPU reassembly: packed shard rows -> O[0, head, token, :]
@@ -893,18 +960,19 @@ void release_device_tables(const svd_plan* P) {
 }
 
 template <int D>
-static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const void* k,
-                      const void* v, void* o, const int64_t* qs, const int64_t* ks,
-                      const int64_t* vs, const int64_t* os, int32_t batch, int32_t head_dim,
-                      cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0,
-                      const int32_t* o_head_map = nullptr) {
+static int launch_fwd(const svd_plan* P, DeviceTables* T, const svd_fwd_args& a, cudaStream_t stream,
+                      void* const* peers = nullptr, int n_peers = 0) {
   using C = KCfg<D>;
   CUtensorMap mq, mk, mv;
   const int64_t N = P->grid.n, H = P->n_heads;
+  const int64_t Hin = a.in_heads > 0 ? a.in_heads : H;
+  const int batch = a.batch, head_dim = a.head_dim;
+  void* o = a.o;
+  const int64_t* os = a.o_strides;
   int st;
-  if ((st = make_tmap(&mq, q, qs, batch, H, N, D, "q"))) return st;
-  if ((st = make_tmap(&mk, k, ks, batch, H, N, D, "k"))) return st;
-  if ((st = make_tmap(&mv, v, vs, batch, H, N, D, "v"))) return st;
+  if ((st = make_tmap(&mq, a.q, a.q_strides, batch, Hin, N, D, "q"))) return st;
+  if ((st = make_tmap(&mk, a.k, a.k_strides, batch, Hin, N, D, "k"))) return st;
+  if ((st = make_tmap(&mv, a.v, a.v_strides, batch, Hin, N, D, "v"))) return st;
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -933,7 +1001,12 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const void* q, const v
   prm.packed = P->sharded ? 1 : 0;
   prm.scale_log2 = float(1.4426950408889634 / std::sqrt(double(head_dim)));
   prm.n_peers = n_peers;
-  prm.o_head_map = o_head_map;
+  prm.o_head_map = a.o_head_map;
+  prm.nonfinite = reinterpret_cast<int*>(a.nonfinite);
+  prm.in_head_map = a.in_head_map;
+  prm.row_stats = a.row_stats;
+  prm.stats_heads = a.row_stats ? a.stats_heads : 0;
+  prm.n_tiles128 = int((N + 127) / 128);
   if (P->n_split_groups > 0) {
     const size_t rows = size_t(P->n_split_groups) * size_t(P->max_split_parts) * 256;
     prm.split_o = static_cast<float*>(T->split_scratch);
@@ -962,36 +1035,79 @@ extern "C" {
 
 const char* svd_version(void) { return "svdit_b200 0.1.0 sm_100a tcgen05/TMA"; }
 
+static int check_args(const svd_plan* P, const svd_fwd_args* a) {
+  if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
+  if (!a) return fail(SVD_ERR_CONFIG, "args is NULL");
+  if (a->dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
+  if (a->head_dim < 1 || a->head_dim > a->tensor_dim)
+    return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
+  if (a->batch < 1) return fail(SVD_ERR_SHAPE, "batch must be >= 1");
+  if (a->in_heads < 0) return fail(SVD_ERR_SHAPE, "in_heads must be >= 0");
+  if (a->in_heads > 0 && a->in_heads != P->n_heads && !a->in_head_map)
+    return fail(SVD_ERR_CONFIG, "in_heads differs from the plan's heads: give in_head_map");
+  if (a->row_stats && (a->stats_heads < 1 || a->stats_heads > P->n_heads))
+    return fail(SVD_ERR_CONFIG, "stats_heads must be in [1, plan heads]");
+  if (!a->q || !a->k || !a->v) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
+  if (a->tensor_dim != 64 && a->tensor_dim != 128)
+    return fail(SVD_ERR_UNSUPPORTED,
+                "tensor_dim " + std::to_string(a->tensor_dim) + " unsupported (64 or 128; pad)");
+  return SVD_OK;
+}
+
+int svd_attn_fwd_args(const svd_plan* P, const svd_fwd_args* a, void* stream) {
+  int st = check_args(P, a);
+  if (st) return st;
+  if (P->sharded && a->batch != 1) return fail(SVD_ERR_UNSUPPORTED, "shard plans run with batch 1");
+  if (P->sharded && a->o_head_map) return fail(SVD_ERR_UNSUPPORTED, "shard plans write packed rows");
+  if (!a->o) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
+  if (a->o_strides[3] != 1 || (a->o_strides[2] * 2) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(a->o) & 15) != 0)
+    return fail(SVD_ERR_UNSUPPORTED, "o: rows must be contiguous and 16-byte aligned");
+  DeviceTables* T = nullptr;
+  if ((st = ensure_device_tables(P, &T))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return a->tensor_dim == 64 ? launch_fwd<64>(P, T, *a, s) : launch_fwd<128>(P, T, *a, s);
+}
+
+static svd_fwd_args make_args(const void* q, const void* k, const void* v, void* o, const int64_t* qs,
+                              const int64_t* ks, const int64_t* vs, const int64_t* os, int32_t batch,
+                              int32_t head_dim, int32_t tensor_dim, int32_t dtype) {
+  svd_fwd_args a{};
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.o = o;
+  for (int i = 0; i < 4; ++i) {
+    a.q_strides[i] = qs[i];
+    a.k_strides[i] = ks[i];
+    a.v_strides[i] = vs[i];
+    a.o_strides[i] = os[i];
+  }
+  a.batch = batch;
+  a.head_dim = head_dim;
+  a.tensor_dim = tensor_dim;
+  a.dtype = dtype;
+  return a;
+}
+
+int svd_attn_fwd_v2(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
+                    const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+                    const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
+                    int32_t dtype, const int32_t* o_head_map, int32_t* nonfinite, void* stream) {
+  if (!q_strides || !k_strides || !v_strides || !o_strides) return fail(SVD_ERR_CONFIG, "NULL strides");
+  svd_fwd_args a = make_args(q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch, head_dim,
+                             tensor_dim, dtype);
+  a.o_head_map = o_head_map;
+  a.nonfinite = nonfinite;
+  return svd_attn_fwd_args(P, &a, stream);
+}
+
 int svd_attn_fwd_ex(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
                     const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
                     const int64_t* o_strides, int32_t batch, int32_t head_dim, int32_t tensor_dim,
                     int32_t dtype, const int32_t* o_head_map, void* stream) {
-  if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
-  if (dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
-  if (head_dim < 1 || head_dim > tensor_dim)
-    return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
-  if (batch < 1) return fail(SVD_ERR_SHAPE, "batch must be >= 1");
-  if (P->sharded && batch != 1) return fail(SVD_ERR_UNSUPPORTED, "shard plans run with batch 1");
-  if (P->sharded && o_head_map) return fail(SVD_ERR_UNSUPPORTED, "shard plans write packed rows");
-  if (!q || !k || !v || !o) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
-  if (o_strides[3] != 1 || (o_strides[2] * 2) % 16 != 0 ||
-      (reinterpret_cast<uintptr_t>(o) & 15) != 0)
-    return fail(SVD_ERR_UNSUPPORTED, "o: rows must be contiguous and 16-byte aligned");
-  DeviceTables* T = nullptr;
-  int st = ensure_device_tables(P, &T);
-  if (st) return st;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (tensor_dim) {
-    case 64:
-      return launch_fwd<64>(P, T, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch,
-                            head_dim, s, nullptr, 0, o_head_map);
-    case 128:
-      return launch_fwd<128>(P, T, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch,
-                             head_dim, s, nullptr, 0, o_head_map);
-    default:
-      return fail(SVD_ERR_UNSUPPORTED,
-                  "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
-  }
+  return svd_attn_fwd_v2(P, q, k, v, o, q_strides, k_strides, v_strides, o_strides, batch, head_dim,
+                         tensor_dim, dtype, o_head_map, nullptr, stream);
 }
 
 int svd_attn_fwd(const svd_plan* P, const void* q, const void* k, const void* v, void* o,
@@ -1062,34 +1178,41 @@ int svd_attn_fwd_peers(const svd_plan* P, const void* q, const void* k, const vo
                        const int64_t* k_strides, const int64_t* v_strides,
                        const int64_t* o_strides, int32_t batch, int32_t head_dim,
                        int32_t tensor_dim, int32_t dtype, void* stream) {
-  if (!P) return fail(SVD_ERR_CONFIG, "plan is NULL");
-  if (dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
   if (n_peers < 1 || n_peers > kMaxPeers || !o_peers)
     return fail(SVD_ERR_CONFIG, "n_peers must be in [1, " + std::to_string(kMaxPeers) + "]");
-  if (head_dim < 1 || head_dim > tensor_dim)
-    return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
-  if (batch < 1) return fail(SVD_ERR_SHAPE, "batch must be >= 1");
-  if (!q || !k || !v) return fail(SVD_ERR_CONFIG, "NULL tensor pointer");
+  if (!q_strides || !k_strides || !v_strides || !o_strides) return fail(SVD_ERR_CONFIG, "NULL strides");
+  svd_fwd_args a = make_args(q, k, v, o_peers[0], q_strides, k_strides, v_strides, o_strides, batch,
+                             head_dim, tensor_dim, dtype);
+  int st = check_args(P, &a);
+  if (st) return st;
   if (o_strides[3] != 1 || (o_strides[2] * 2) % 16 != 0)
     return fail(SVD_ERR_UNSUPPORTED, "o: rows must be contiguous and 16-byte aligned");
   for (int r = 0; r < n_peers; ++r)
     if (!o_peers[r] || (reinterpret_cast<uintptr_t>(o_peers[r]) & 15) != 0)
       return fail(SVD_ERR_UNSUPPORTED, "peer O pointers must be non-NULL and 16-byte aligned");
   DeviceTables* T = nullptr;
-  int st = ensure_device_tables(P, &T);
-  if (st) return st;
+  if ((st = ensure_device_tables(P, &T))) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (tensor_dim) {
-    case 64:
-      return launch_fwd<64>(P, T, q, k, v, o_peers[0], q_strides, k_strides, v_strides, o_strides,
-                            batch, head_dim, s, o_peers, n_peers);
-    case 128:
-      return launch_fwd<128>(P, T, q, k, v, o_peers[0], q_strides, k_strides, v_strides, o_strides,
-                             batch, head_dim, s, o_peers, n_peers);
-    default:
-      return fail(SVD_ERR_UNSUPPORTED,
-                  "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
+  return tensor_dim == 64 ? launch_fwd<64>(P, T, a, s, o_peers, n_peers)
+                          : launch_fwd<128>(P, T, a, s, o_peers, n_peers);
+}
+
+int svd_peer_barrier(int32_t* const* flags, int32_t n_peers, int32_t rank, int32_t epoch,
+                     int32_t* timed_out, double timeout_s, void* stream) {
+  if (!flags || n_peers < 1 || n_peers > kMaxPeers || rank < 0 || rank >= n_peers)
+    return fail(SVD_ERR_CONFIG, "peer barrier: bad flags / n_peers / rank");
+  PeerFlags pf{};
+  for (int r = 0; r < n_peers; ++r) {
+    if (!flags[r] || (reinterpret_cast<uintptr_t>(flags[r]) & 3) != 0)
+      return fail(SVD_ERR_CONFIG, "peer barrier: flag arrays must be non-NULL and 4-byte aligned");
+    pf.f[r] = flags[r];
   }
+  const uint64_t tns = timeout_s > 0 ? uint64_t(timeout_s * 1e9) : uint64_t(30e9);
+  svd_peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(pf, n_peers, rank, epoch,
+                                                                         timed_out, tns);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "svd_peer_barrier_kernel launch");
+  return SVD_OK;
 }
 
 int svd_head_sqdiff(const void* a, const void* b, const int64_t* as, const int64_t* bs,

@@ -321,10 +321,12 @@ static int cuda_fail(cudaError_t e, const char* what) {
   return fail(SVD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// row_pass: run pass 0 (row statistics); false = stats already hold them
+// (svd_fwd_args.row_stats of a forward launch), only the key-sum pass runs
 template <int D>
 static int launch(const void* q, const void* k, const int64_t* qs, const int64_t* ks, int batch,
                   int heads, int64_t n, int head_dim, int block_size, float* stats, double* key_acc,
-                  double* mass, cudaStream_t stream) {
+                  double* mass, cudaStream_t stream, bool row_pass = true) {
   using C = Cfg<D>;
   CUtensorMap mq, mk;
   int st;
@@ -350,7 +352,7 @@ static int launch(const void* q, const void* k, const int64_t* qs, const int64_t
   p.stats = stats;
   p.key_acc = key_acc;
   const dim3 grid(unsigned((p.n_tiles + 1) / 2), unsigned(heads), unsigned(batch));
-  key_mass_kernel<D, 0><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, p);
+  if (row_pass) key_mass_kernel<D, 0><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, p);
   key_mass_kernel<D, 1><<<grid, kThreads, C::kSmemBytes, stream>>>(mk, mq, p);
   const int64_t n_bh = int64_t(batch) * heads;
   const int nb = int((n + block_size - 1) / block_size);
@@ -402,6 +404,41 @@ int svd_block_key_mass(const void* q, const void* k, const int64_t* q_strides, c
     case 128:
       return km::launch<128>(q, k, q_strides, k_strides, batch, heads, n_tokens, head_dim, block_size,
                              stats, key_acc, mass, s);
+    default:
+      return fail(SVD_ERR_UNSUPPORTED,
+                  "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");
+  }
+}
+
+int svd_block_key_mass_from_stats(const void* q, const void* k, const int64_t* q_strides,
+                                  const int64_t* k_strides, int32_t batch, int32_t heads,
+                                  int64_t n_tokens, int32_t head_dim, int32_t tensor_dim,
+                                  int32_t block_size, int32_t dtype, const float* row_stats,
+                                  void* workspace, int64_t workspace_bytes, double* mass,
+                                  void* stream) {
+  if (!q || !k || !mass || !workspace || !row_stats) return fail(SVD_ERR_CONFIG, "NULL pointer");
+  if (dtype != 0) return fail(SVD_ERR_UNSUPPORTED, "only bf16 (dtype 0) is supported");
+  if (batch < 1 || heads < 1 || n_tokens < 1) return fail(SVD_ERR_SHAPE, "bad shape");
+  if (n_tokens > (int64_t(1) << 30)) return fail(SVD_ERR_UNSUPPORTED, "n_tokens too large");
+  if (block_size < 1) return fail(SVD_ERR_CONFIG, "block_size must be >= 1");
+  if (head_dim < 1 || head_dim > tensor_dim)
+    return fail(SVD_ERR_SHAPE, "head_dim must be in [1, tensor_dim]");
+  const int64_t need = svd_key_mass_workspace(batch, heads, n_tokens);
+  if (workspace_bytes < need)
+    return fail(SVD_ERR_CONFIG, "workspace too small: need " + std::to_string(need) + " bytes");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0 || (reinterpret_cast<uintptr_t>(row_stats) & 15) != 0)
+    return fail(SVD_ERR_UNSUPPORTED, "workspace and row_stats must be 16-byte aligned");
+  const int64_t tiles = (n_tokens + 127) / 128;
+  float* stats = const_cast<float*>(row_stats);  // read only by the key-sum pass
+  double* key_acc = reinterpret_cast<double*>(static_cast<float*>(workspace) + int64_t(batch) * heads * tiles * 256);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (tensor_dim) {
+    case 64:
+      return km::launch<64>(q, k, q_strides, k_strides, batch, heads, n_tokens, head_dim, block_size,
+                            stats, key_acc, mass, s, false);
+    case 128:
+      return km::launch<128>(q, k, q_strides, k_strides, batch, heads, n_tokens, head_dim, block_size,
+                             stats, key_acc, mass, s, false);
     default:
       return fail(SVD_ERR_UNSUPPORTED,
                   "tensor_dim " + std::to_string(tensor_dim) + " unsupported (64 or 128; pad)");

@@ -3,8 +3,8 @@
 // reference (svdit 0.1.0):
 //   layout.py:26-80    TokenLayout validation, total_tokens, frame_of
 //   layout.py:135-158  block_grid (bounds / has_text / mixed / frame_index)
-//   patterns.py:334-339 frame_period (Python round(): half-to-even)
-//   patterns.py:377-417 build_mask (5 modes, forced rows/cols, empty-row error)
+//   patterns.py:176-181 frame_period (Python round(): half-to-even)
+//   patterns.py:219-259 build_mask (5 modes, forced rows/cols, empty-row error)
 //   attention.py:164-183 group_heads (first-occurrence order, ascending heads,
 //                         keyed on full PatternSpec equality)
 // and then lowers each group's block mask to the kernel schedule: 64-token
@@ -93,7 +93,7 @@ static int make_grid(const svd_layout* L, Grid* g) {
   return SVD_OK;
 }
 
-// patterns.py:334-339 frame_period: max(1, round(tpf / size)), banker's rounding
+// patterns.py:176-181 frame_period: max(1, round(tpf / size)), banker's rounding
 static int64_t frame_period(const svd_layout* L) {
   const double ratio = double(L->tokens_per_frame) / double(L->block_size);
   const int64_t r = int64_t(std::nearbyint(ratio));  // FE_TONEAREST = half-to-even
@@ -101,7 +101,7 @@ static int64_t frame_period(const svd_layout* L) {
 }
 
 // ---------------------------------------------------------------- specs
-// patterns.py:225-233 PatternSpec.__post_init__ (validation + stripe normalisation)
+// patterns.py:67-75 PatternSpec.__post_init__ (validation + stripe normalisation)
 static int normalise_spec(const svd_spec* s, NormSpec* out) {
   if (!s) return fail(SVD_ERR_CONFIG, "spec is NULL");
   if (s->mode < 0 || s->mode > 4)
@@ -126,7 +126,7 @@ static int normalise_spec(const svd_spec* s, NormSpec* out) {
   return SVD_OK;
 }
 
-// patterns.py:377-417 build_mask.  active must hold nb*nb bytes.
+// patterns.py:219-259 build_mask.  active must hold nb*nb bytes.
 static int build_mask(const NormSpec& spec, const Grid& g, const svd_layout* L, uint8_t* active,
                       bool* is_skip) {
   const int64_t nb = g.nb;
@@ -177,13 +177,13 @@ static int build_mask(const NormSpec& spec, const Grid& g, const svd_layout* L, 
     if (spec.include_diagonal)
       for (int64_t i = 0; i < nb; ++i) active[i * nb + i] = 1;
   }
-  // layout.py:119-122 forced = has_text | mixed; patterns.py:411-413
+  // layout.py:119-122 forced = has_text | mixed; patterns.py:253-255
   for (int64_t b = 0; b < nb; ++b) {
     if (!(g.has_text[b] || g.mixed[b])) continue;
     std::memset(active + b * nb, 1, size_t(nb));
     for (int64_t i = 0; i < nb; ++i) active[i * nb + b] = 1;
   }
-  // patterns.py:414-416
+  // patterns.py:256-258
   for (int64_t i = 0; i < nb; ++i) {
     bool any = false;
     for (int64_t j = 0; j < nb && !any; ++j) any = active[i * nb + j];
@@ -683,7 +683,7 @@ int svd_plan_group_nnz(const svd_plan* P, int32_t g, int64_t* nnz) {
   return SVD_OK;
 }
 
-// patterns.py:363-366 active_key_blocks(qb) = flatnonzero(active[qb]), per row
+// patterns.py:205-208 active_key_blocks(qb) = flatnonzero(active[qb]), per row
 int svd_plan_group_csr(const svd_plan* P, int32_t g, int64_t* row_ptr, int64_t* col_idx) {
   if (!P || g < 0 || g >= int32_t(P->groups.size())) return fail(SVD_ERR_CONFIG, "bad group index");
   const Group& grp = P->groups[g];

@@ -39,18 +39,26 @@ def gathered_row_maps(plan: LayerPlan, world: int, max_item_tiles: int = 0):
 class PeerShardedLayer:
     """One layer over `world` ranks with the reassembly fused into the kernel.
 
-    Every rank owns an O buffer [1, H, N, D]; the buffers are exchanged once
-    as CUDA IPC handles over the process group and mapped into every rank
-    (NVLink peer memory between GPUs).  Each rank launches its shard of the
-    plan with svd_attn_fwd_peers: the kernel epilogue stores each finished
-    row into all `world` O buffers, so the transfer overlaps the attention
-    math tile by tile and no all-gather / unpack runs afterwards.  A
-    stream sync + process-group barrier closes the step (every rank's O is
-    then complete).
+    Every rank owns one device buffer holding two O buffers [B, H, N, D]
+    (double-buffered across steps) and an int32 flag array; the buffers are
+    exchanged once as CUDA IPC handles over the process group and mapped into
+    every rank (NVLink peer memory between GPUs).  A step launches this rank's
+    shard with svd_attn_fwd_peers — the kernel epilogue stores each finished
+    row into the step's O buffer of all `world` ranks, so the transfer
+    overlaps the attention math tile by tile and no all-gather / unpack runs
+    — then svd_peer_barrier, a stream-ordered barrier over the flag arrays:
+    no host synchronisation and no process-group call on the data path.
+
+    Buffer lifetime: the O returned by step t is complete once the caller's
+    stream passes that step's barrier, and stays valid until the step after
+    next (t + 2) starts writing the same buffer.  Work the caller enqueues on
+    this stream between the calls (e.g. consuming step t's O before calling
+    step t + 1) is ordered before every peer's t + 2 stores by the t + 1
+    barrier.
     """
 
     def __init__(self, plan: LayerPlan, world: int, rank: int, head_dim: int, device, shape,
-                 max_item_tiles: int | None = None, partition: str = "heads"):
+                 max_item_tiles: int | None = None, partition: str = "heads", timeout_s: float = 30.0):
         import torch
         import torch.distributed as dist
 
@@ -59,6 +67,7 @@ class PeerShardedLayer:
         self.rank = rank
         self.head_dim = head_dim
         self.device = device
+        self.timeout_s = float(timeout_s)
         # a shard view (split-KV balanced) for N > 1, the plain plan for one rank
         # unless a split cap is forced (tests).  "heads": contiguous head
         # ranges of equal cost, so a rank's inputs are its own heads only
@@ -69,57 +78,88 @@ class PeerShardedLayer:
         # heads whose Q/K/V this rank reads (about H / world of them for "heads")
         self.heads = self.shard.shard_heads() if self.shard is not plan else tuple(range(plan.n_heads))
         self._inputs = None
-        self.out = torch.empty(shape, dtype=torch.bfloat16, device=device)
+        # one allocation per rank: [O buffer 0 | O buffer 1 | flags int32[8]]
+        o_elems = 1
+        for s in shape:
+            o_elems *= int(s)
+        o_bytes = (o_elems * 2 + 255) // 256 * 256
+        self._buf = torch.zeros(2 * o_bytes + 256, dtype=torch.uint8, device=device)
+        self.outs = [self._buf[i * o_bytes: i * o_bytes + o_elems * 2].view(torch.bfloat16).view(*shape)
+                     for i in range(2)]
+        self.flags = self._buf[2 * o_bytes: 2 * o_bytes + 32].view(torch.int32)
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+        self._o_bytes = o_bytes
         off = nat.c_int64(0)
-        buf = (nat.c_uint8 * 64)()
-        nat.check(nat.lib().svd_ipc_export(nat.c_void_p(self.out.data_ptr()), buf, nat.ctypes.byref(off)))
-        handle = bytes(buf)
+        hbuf = (nat.c_uint8 * 64)()
+        nat.check(nat.lib().svd_ipc_export(nat.c_void_p(self._buf.data_ptr()), hbuf, nat.ctypes.byref(off)))
         gathered = [None] * world
         if world > 1:
-            dist.all_gather_object(gathered, (rank, handle, int(off.value)))
+            dist.all_gather_object(gathered, (rank, bytes(hbuf), int(off.value)))
         else:
-            gathered = [(rank, handle, int(off.value))]
+            gathered = [(rank, bytes(hbuf), int(off.value))]
         self._opened = []
-        ptrs = []
+        bases = []
         for r, h, o in sorted(gathered):
             if r == rank:
-                ptrs.append(self.out.data_ptr())
+                bases.append(self._buf.data_ptr())
                 continue
             p = nat.c_void_p()
             hb = (nat.c_uint8 * 64).from_buffer_copy(h)
             nat.check(nat.lib().svd_ipc_import(hb, o, nat.ctypes.byref(p)))
             self._opened.append((p.value, o))
-            ptrs.append(p.value)
-        self.peer_ptrs = (nat.c_void_p * world)(*ptrs)
+            bases.append(p.value)
+        self.peer_ptrs = [(nat.c_void_p * world)(*[b + i * o_bytes for b in bases]) for i in range(2)]
+        self.flag_ptrs = (nat.c_void_p * world)(*[b + 2 * o_bytes for b in bases])
+        self.step = 0
+        torch.cuda.synchronize(device)
+        if world > 1:
+            dist.barrier()  # every rank's flags are zero before any step runs
+
+    @property
+    def out(self):
+        """The O buffer of the latest step (buffer 0 before the first step)."""
+        return self.outs[(self.step - 1) % 2] if self.step else self.outs[0]
 
     def __call__(self, q, k, v, out=None, kernel_events=None):
-        """Run this rank's shard; returns this rank's complete O (all rows)."""
+        """Run this rank's shard and the step barrier; returns this rank's
+        complete O (all rows) — stream-ordered, no host synchronisation."""
         import torch
 
+        b = self.step % 2
         stream = torch.cuda.current_stream(self.device)
-        if kernel_events is not None:
-            kernel_events[0].record(stream)
-        st = [nat.i64x4(t.stride()) for t in (q, k, v)]
-        nat.check(nat.lib().svd_attn_fwd_peers(
-            self.shard.handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
-            nat.c_void_p(v.data_ptr()), self.peer_ptrs, self.world, st[0], st[1], st[2],
-            nat.i64x4(self.out.stride()), 1, int(self.head_dim), int(q.shape[-1]), 0,
-            nat.c_void_p(stream.cuda_stream)))
-        if kernel_events is not None:
-            kernel_events[1].record(stream)
-        if self.world > 1:
-            import torch.distributed as dist
+        with torch.cuda.device(self.device):
+            if kernel_events is not None:
+                kernel_events[0].record(stream)
+            st = [nat.i64x4(t.stride()) for t in (q, k, v)]
+            nat.check(nat.lib().svd_attn_fwd_peers(
+                self.shard.handle, nat.c_void_p(q.data_ptr()), nat.c_void_p(k.data_ptr()),
+                nat.c_void_p(v.data_ptr()), self.peer_ptrs[b], self.world, st[0], st[1], st[2],
+                nat.i64x4(self.outs[b].stride()), 1, int(self.head_dim), int(q.shape[-1]), 0,
+                nat.c_void_p(stream.cuda_stream)))
+            if kernel_events is not None:
+                kernel_events[1].record(stream)
+            if self.world > 1:
+                nat.check(nat.lib().svd_peer_barrier(
+                    self.flag_ptrs, self.world, self.rank, nat.c_int32((self.step + 1) & 0xFFFFFFFF).value,
+                    nat.c_void_p(self.timed_out.data_ptr()), self.timeout_s, nat.c_void_p(stream.cuda_stream)))
+        self.step += 1
+        res = self.outs[b]
+        if out is not None and out.data_ptr() != res.data_ptr():
+            out.copy_(res)
+            return out
+        return res
 
-            stream.synchronize()
-            dist.barrier()
-        if out is not None and out.data_ptr() != self.out.data_ptr():
-            out.copy_(self.out)
-        return self.out
+    def check(self) -> None:
+        """Raise if a step barrier timed out (a peer never arrived).  Reads a
+        device flag: synchronises the stream."""
+        if int(self.timed_out.item()) != 0:
+            raise nat.NativeError("peer barrier timed out: a rank did not finish its step")
 
     def e2e(self, hq, hk, hv, hout, groups=None):
         """End-to-end step from pinned host buffers: H2D of the heads this
-        rank reads, the fused shard kernel (rows land in every rank's O), D2H
-        of those heads of O (the ranks' head sets cover every head)."""
+        rank reads, the fused shard kernel (rows land in every rank's O) and
+        the step barrier, D2H of those heads of O (the ranks' head sets cover
+        every head)."""
         import torch
 
         if self._inputs is None or self._inputs[0].shape != hq.shape:
@@ -138,6 +178,14 @@ class PeerShardedLayer:
         B, _, N, d = shape
         h = len(self.heads)
         return 3 * B * h * N * d * 2, B * h * N * d * 2
+
+    def nvlink_bytes(self, tensor_dim: int) -> int:
+        """Bytes this rank's epilogue stores into its peers' O per step: every
+        row it computes, once per other rank (bf16 [tensor_dim])."""
+        if self.world == 1:
+            return 0
+        heads, _ = self.shard.shard_rows()
+        return int(len(heads)) * tensor_dim * 2 * (self.world - 1)
 
     def close(self):
         for p, o in self._opened:

@@ -104,7 +104,12 @@ def test_cost_model_conventions():
     assert 0 < short < long < 1
     assert round(short, 4) == 0.7099 and round(long, 4) == 0.8659
     m = S.B200LatencyModel(launch_ms=0.01, ms_per_tile={128: 1e-5})
-    assert m.effective_sparsity(500, 1000, 128) == pytest.approx(1 - (0.01 + 0.005) / (0.01 + 0.01))
+    # per head: the whole-launch constant is left out of the ratio
+    assert m.effective_sparsity(500, 1000, 128) == pytest.approx(0.5)
+    # head dims the kernel runs zero-padded use the 64 / 128 fits
+    m2 = S.B200LatencyModel(ms_per_tile={64: 1e-5, 128: 2e-5})
+    assert m2.effective_sparsity(250, 1000, 32) == pytest.approx(0.75)
+    assert m2.effective_sparsity(250, 1000, 96) == pytest.approx(0.75)
 
 
 def test_layer_plan_flops_match_reference_convention():
@@ -321,3 +326,31 @@ def test_plan_schedule_matches_masks(block):
             want = set().union(*(need[s] for s in it[4:8] if s >= 0))
             assert got == want
     assert n_all > 0  # the FULL head's interior tiles at least
+
+
+def test_edited_groups_are_lowered_from_their_own_masks():
+    """a group rebuilt with dataclasses.replace(g, mask=...) keeps
+    g.plan; the fused call must lower the edited mask, not reuse the plan."""
+    import dataclasses
+
+    from paper_2506_03065_b200.attention import _mask_plan, _plan_for_groups
+
+    grid = S.block_grid(S.TokenLayout(0, 8, 256, 64))
+    groups = S.group_heads([S.diagonal_spec(1), S.full_spec()], grid)
+    plan = groups[0].plan
+    assert _plan_for_groups(groups, 2, grid.layout.total_tokens) is plan
+    # masks handed out by group_heads are shared, so they are read-only
+    assert not groups[0].mask.active.flags.writeable
+    with pytest.raises(ValueError):
+        groups[0].mask.active[0, -1] = True
+    edited = dataclasses.replace(groups[0], mask=S.BlockMask(grid=grid, active=np.ones_like(groups[0].mask.active)))
+    other = _plan_for_groups([edited, groups[1]], 2, grid.layout.total_tokens)
+    assert other is not plan
+    assert other.group_mask(0).all()
+    # writable masks are keyed by content: an in-place edit gives a new plan
+    m = S.build_mask(S.diagonal_spec(1), grid)
+    p1 = _mask_plan(m, 1)
+    assert _mask_plan(m, 1) is p1
+    m.active[0, :] = True
+    p2 = _mask_plan(m, 1)
+    assert p2 is not p1 and p2.group_mask(0)[0].all()

@@ -156,3 +156,75 @@ def test_resolve_stripes_head_subset():
         if order[1] - order[2] > 1e-4:
             assert full[h] == top_stripes(want[h], 2)
     assert ev.resolve_stripes(q, k, []) == {}
+
+
+def test_candidate_evaluator_one_launch_path_matches_first_evaluation():
+    """With the stripe columns frozen (every evaluation after a layer's first,
+    search.py:338-346) the four candidates run as one 4H-head launch; its
+    outputs (hence MSEs, losses, choices) equal the first evaluation's
+    (FULL + diagonal + multi-diagonal launch, key-sum pass, stripe launch)
+    bit for bit."""
+    import torch
+
+    from paper_2506_03065_b200.calibrate import CandidateEvaluator
+
+    lay = (96, 16, 250, 64)
+    og = O.block_grid(*lay)
+    g = S.block_grid(S.TokenLayout(*lay))
+    for d in (64, 128):
+        q, k, v = _inputs(17, 5, og.n, d, 3.0)
+        ev = CandidateEvaluator(g, S.SearchParams(lam=0.05, epsilon=1.0))
+        first = ev.evaluate(q, k, v)
+        again = ev.evaluate(q, k, v, stripes=first.stripes)
+        np.testing.assert_array_equal(first.mse, again.mse)
+        assert first.choices == again.choices
+        assert torch.equal(first.selected, again.selected)
+
+
+def test_key_mass_from_forward_row_stats():
+    """The FULL launch's per-row (-m, 1/l) drive block_key_mass's key-sum pass:
+    the masses equal the two-pass kernel's within 1e-6 and the oracle's
+    within 2e-5 (attention.py:108-146), for d = 64 / 128 and a ragged tail."""
+    import torch
+
+    from paper_2506_03065_b200.calibrate import block_key_mass, block_key_mass_from_stats
+
+    for lay, d in (((96, 16, 250, 64), 128), ((0, 7, 300, 64), 64), ((30, 5, 333, 48), 64)):
+        og = O.block_grid(*lay)
+        g = S.block_grid(S.TokenLayout(*lay))
+        H = 3
+        q, k, v = _inputs(19, H, og.n, d, 2.0)
+        dq, dk, dv = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v))
+        plan = S.plan_for_assignment([S.full_spec()] * H, g.layout)
+        T = (og.n + 127) // 128
+        stats = torch.empty(H, T, 2, 128, dtype=torch.float32, device="cuda")
+        stats[:, :, 0].fill_(float("-inf"))
+        stats[:, :, 1].zero_()
+        out = torch.empty_like(dq)
+        plan.forward(dq, dk, dv, out, head_dim=d, row_stats=stats, stats_heads=H)
+        got = block_key_mass_from_stats(dq, dk, g, stats, head_dim=d).cpu().numpy()
+        two_pass = block_key_mass(dq, dk, g).cpu().numpy()
+        want = O.block_key_mass(q, k, og)
+        np.testing.assert_allclose(got, two_pass, atol=1e-6)
+        np.testing.assert_allclose(got, want, atol=2e-5)
+        np.testing.assert_allclose(got.sum(axis=-1), 1.0, atol=1e-5)
+
+
+def test_input_head_map_reads_shared_qkv():
+    """A plan whose heads are (copy, head) pairs over one q/k/v (in_head_map)
+    gives, per copy, exactly the plain launch's output."""
+    import torch
+
+    lay = (96, 16, 250, 64)
+    g = S.block_grid(S.TokenLayout(*lay))
+    H, d = 3, 128
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn(1, H, 4096, d, device="cuda", generator=gen).to(torch.bfloat16) for _ in range(3))
+    specs = [S.full_spec(), S.diagonal_spec(1), S.vertical_stripe_spec(stripes=(2, 9))]
+    ref = torch.empty_like(q)
+    S.plan_for_assignment(specs, g.layout).forward(q, k, v, ref, head_dim=d)
+    big = S.plan_for_assignment(specs + specs, g.layout)
+    out = torch.empty(1, 2 * H, 4096, d, dtype=torch.bfloat16, device="cuda")
+    in_map = torch.arange(H, dtype=torch.int32, device="cuda").repeat(2)
+    big.forward(q, k, v, out, head_dim=d, in_head_map=in_map)
+    assert torch.equal(out[:, :H], ref) and torch.equal(out[:, H:], ref)

@@ -49,11 +49,20 @@ def _worker(rank, world, port, path, d):
         layer = PeerShardedLayer(plan, world, rank, d, dev, tuple(q.shape))
         oks = []
         for _ in range(2):
-            layer.out.fill_(float("nan"))
+            for o in layer.outs:
+                o.fill_(float("nan"))
+            torch.cuda.synchronize()
             dist.barrier()
             out = layer(q, k, v)
             torch.cuda.synchronize()
             oks.append(bool(torch.equal(out, ref)))
+        # back to back, no host barrier: the stream-ordered peer barrier alone
+        # orders the steps; each returned buffer must hold the full result
+        outs = [layer(q, k, v) for _ in range(4)]
+        got = [bool(torch.equal(o, ref)) for o in outs[-2:]]
+        torch.cuda.synchronize()
+        oks.extend(got)
+        layer.check()
         # end to end: each rank copies in its own head range, copies out that range of O
         hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
         hout = torch.full(q.shape, float("nan"), dtype=torch.bfloat16).pin_memory()

@@ -169,3 +169,21 @@ def test_oracle_layer_finish_matches_reference():
     np.testing.assert_allclose(O.layer_finish(w, g["x"], g["attn"]), g["finish"], rtol=0, atol=1e-5)
     # layer_forward = layer_finish(layer_qkv -> fused attention)
     np.testing.assert_array_equal(g["finish"], g["forward"])
+
+
+def test_attention_rows_equals_streaming_oracle():
+    """oracle.attention_rows (one softmax over a block's active keys, used
+    for the full-size GPU parity samples) equals the streaming recurrence of
+    attention.py:57-98 (oracle.sparse_attention_rows) on text / frame-border /
+    tail blocks of a text layout, for every mode, at q x1 and q x8."""
+    og = O.block_grid(96, 8, 250, 64)
+    specs = [O.full_spec(), O.diagonal_spec(1), O.multi_diagonal_spec(), O.vertical_stripe_spec(stripes=(3, 20))]
+    for qscale in (1.0, 8.0):
+        q, k, v = O.random_qkv(5, 1, 1, og.n, 32)
+        q = q * np.float32(qscale)
+        for spec in specs:
+            active = O.build_mask(spec, og)
+            qbs = [0, 1, 4, 11, og.n_blocks - 1]
+            a = O.attention_rows(q, k, v, active, og.bounds, qbs)
+            b = O.sparse_attention_rows(q, k, v, active, og.bounds, qbs)
+            np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)

@@ -233,3 +233,23 @@ def test_head_partition_is_balanced_and_head_local():
         assert max(len(x) for x in sets) < max(len(x) for x in items_sets)  # vs LPT over items
     with pytest.raises(S.ConfigError):
         plan.shard(2, 0, partition="rows")
+
+
+@pytest.mark.parametrize("config", ["synthetic4k", "cogvideo", "hunyuan", "wan"])
+def test_bench_assignment_same_in_both_arms(config):
+    """bench.assignment_for built from the product's spec constructors (GPU
+    arm) and from the oracle's (CPU arms) gives the same grouping and
+    bit-identical masks, so both arms time the same layer."""
+    import bench
+
+    cfg = bench.CONFIGS[config]
+    og = O.block_grid(*cfg["layout"])
+    ours = S.group_heads(bench.assignment_for(cfg, S), S.block_grid(S.TokenLayout(*cfg["layout"])))
+    ref = O.group_heads(bench.assignment_for(cfg, O), og)
+    assert [g.heads for g in ours] == [heads for _, heads, _ in ref]
+    for g, (spec, heads, mask) in zip(ours, ref):
+        assert int(g.spec.mode) == int(spec.mode)
+        if mask is None:
+            assert g.mask is None
+        else:
+            np.testing.assert_array_equal(np.asarray(g.mask.active), mask)
