@@ -415,26 +415,45 @@ def _numpy_e2e(S, hq, hk, hv, groups, e2e_bytes):
 
 
 def _search_step(S, layout, q, k, v, stream, dev):
-    """The offline search's per-layer step on the bench layer."""
+    """The offline search's per-layer step on the bench layer (SURVEY §8f rows
+    1-2, search.py:334-372): the first evaluation of a layer (stripe
+    calibration: FULL + diagonal + multi-diagonal launch that also writes the
+    row statistics, the key-sum pass, the stripe launch) and every later one
+    (stripes frozen, search.py:338-346: ONE launch of all four candidates),
+    beside the FULL candidate alone and the stand-alone two-pass key mass."""
     import torch
 
     from paper_2506_03065_b200.calibrate import CandidateEvaluator, block_key_mass
 
     grid = S.block_grid(layout)
     ev = CandidateEvaluator(grid, S.SearchParams())
-    ev.evaluate(q, k, v)  # first call builds the candidate plans
-    a0, a1, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-    a0.record(stream)
+    first = ev.evaluate(q, k, v)  # builds the candidate plans
+    ev.evaluate(q, k, v, stripes=first.stripes)
+    H, d = q.shape[1], q.shape[-1]
+    full_plan = S.plan_for_assignment([S.full_spec()] * H, layout)
+    o = torch.empty_like(q)
+    ev_ = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev_[0].record(stream)
     block_key_mass(q, k, grid)
-    a1.record(stream)
+    ev_[1].record(stream)
     ev.evaluate(q, k, v)
-    b1.record(stream)
+    ev_[2].record(stream)
+    ev.evaluate(q, k, v, stripes=first.stripes)
+    ev_[3].record(stream)
+    full_plan.forward(q, k, v, o, head_dim=d)
+    ev_[4].record(stream)
     torch.cuda.synchronize(dev)
-    return {"block_key_mass_ms": round(a0.elapsed_time(a1), 2),
-            "candidate_evaluation_ms": round(a1.elapsed_time(b1), 2),
-            "what": "calibrate.block_key_mass (two tcgen05 passes) and "
-                    "CandidateEvaluator.evaluate (stripe calibration + FULL / diagonal / "
-                    "multi-diagonal / stripe candidates + per-head fp64 MSE), search.py:334-372"}
+    full_ms = ev_[3].elapsed_time(ev_[4])
+    steady = ev_[2].elapsed_time(ev_[3])
+    return {"block_key_mass_ms": round(ev_[0].elapsed_time(ev_[1]), 2),
+            "first_evaluation_ms": round(ev_[1].elapsed_time(ev_[2]), 2),
+            "candidate_evaluation_ms": round(steady, 2),
+            "full_candidate_alone_ms": round(full_ms, 2),
+            "candidate_evaluation_over_full": round(steady / full_ms, 3),
+            "what": "calibrate.CandidateEvaluator.evaluate: FULL / diagonal / multi-diagonal / stripe "
+                    "candidates as (candidate, head) pairs of one fused launch + per-head fp64 MSE + "
+                    "mode_loss / select_mode (search.py:334-372); first evaluation adds the stripe "
+                    "calibration from the FULL launch's row statistics (key-sum pass only)"}
 
 
 def init_dist():

@@ -322,6 +322,22 @@ int svd_unpack_rows(const int32_t* row_head_dev, const int32_t* row_token_dev, i
  * The projections are plain GEMMs (cuBLAS); these are the streaming passes
  * between them.  All pointers are device pointers, 16-byte aligned. */
 
+/* C[M, N] = A[M, K] . B[K, N] on the tensor cores (tcgen05, fp32 accumulate)
+ * with the block's element-wise step fused into the epilogue.  A, B: bf16
+ * row-major with leading dimensions lda / ldb (elements; the weight B as
+ * stored, [in, out]).  epilogue:
+ *   0 = bf16 out
+ *   1 = bf16 out, RoPE (model.py:169-195) on columns [0, rope_cols): column c
+ *       belongs to head-local column c % head_dim, pair (2i, 2i+1) rotates by
+ *       rope_table[row % n_tokens][i] = (cos, sin) (svd_rope_table)
+ *   2 = bf16 out, exact GELU (model.py:357-359)
+ *   3 = fp32 out + resid (fp32 [M, ldr])
+ *   4 = fp32 out
+ * N, K multiples of 8; out rows 16-byte aligned. */
+int svd_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* out, int64_t ldo, int64_t M,
+             int64_t N, int64_t K, int32_t epilogue, const float* resid, int64_t ldr, const void* rope_table,
+             int32_t rope_cols, int32_t head_dim, int64_t n_tokens, void* stream);
+
 /* LayerNorm without affine over rows of `dim` fp32 values (model.py:352-355),
  * bf16 output y.  resid != NULL fuses the residual add first: x_out = x +
  * resid (fp32, may alias x) and y = LN(x_out).  dim % 4 == 0. */

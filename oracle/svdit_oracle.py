@@ -293,14 +293,18 @@ def attention_rows(q, k, v, active, bounds, qblocks) -> np.ndarray:
     B, H, N, d = q.shape
     scale = 1.0 / np.sqrt(d)
     sizes = np.diff(bounds)
+    kall = np.asarray(k, dtype=np.float64)
+    vall = np.asarray(v, dtype=np.float64)
     outs = []
     for qb in qblocks:
         r0, r1 = int(bounds[qb]), int(bounds[qb + 1])
         kbs = np.flatnonzero(active[qb])
-        cols = np.concatenate([np.arange(bounds[c], bounds[c] + sizes[c]) for c in kbs])
         q64 = np.asarray(q[:, :, r0:r1], dtype=np.float64)
-        k64 = np.asarray(k[:, :, cols], dtype=np.float64)
-        v64 = np.asarray(v[:, :, cols], dtype=np.float64)
+        if len(kbs) == len(sizes):  # every key block active (forced rows, FULL heads)
+            k64, v64 = kall, vall
+        else:
+            cols = np.concatenate([np.arange(bounds[c], bounds[c] + sizes[c]) for c in kbs])
+            k64, v64 = kall[:, :, cols], vall[:, :, cols]
         s = np.matmul(q64, k64.swapaxes(-1, -2)) * scale
         s -= s.max(axis=-1, keepdims=True)
         p = np.exp(s)

@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsvdit_b200.so"
-SOURCES = ["svd_plan.cpp", "svd_attn_fwd.cu", "svd_layer.cu", "svd_key_mass.cu"]
+SOURCES = ["svd_plan.cpp", "svd_attn_fwd.cu", "svd_layer.cu", "svd_key_mass.cu", "svd_gemm.cu"]
 HEADERS = ["svd_plan.h", "svd_ptx.cuh"]
 
 NVCC_FLAGS = [

@@ -171,6 +171,8 @@ SIGNATURES = {
     "svd_rope_apply": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p,
                                c_void_p]),
     "svd_gelu": (c_int, [c_void_p, c_int64, c_void_p]),
+    "svd_gemm": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                         c_int32, c_void_p, c_int64, c_void_p, c_int32, c_int32, c_int64, c_void_p]),
 }
 
 _lib = None

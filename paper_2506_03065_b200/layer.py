@@ -17,9 +17,14 @@ B200 data flow (no split/merge-heads copies):
   q/k/v = strided [B, H, N, d] views of qkv (the attention kernel reads them
   through TMA strides) --attention--> O stored [B, N, H, d] (= merged heads)
   --GEMM, fp32 out--> svd_layernorm(x + proj) --GEMM--> svd_gelu --GEMM, fp32--> + a
-GEMMs are plain cuBLAS (torch.mm, bf16 operands, fp32 accumulation); the
-row / element passes between them are this package's kernels (csrc/svd_layer.cu).
-The residual stream x stays fp32 like the reference's float32 latent.
+The four GEMMs are this package's tcgen05 kernel (csrc/svd_gemm.cu, bf16
+operands, fp32 accumulation in TMEM) with the step after each fused into its
+epilogue: RoPE on the q / k column blocks of the QKV projection, the
+attention residual (a = x + O Wo, fp32), exact GELU after W1 and the MLP
+residual (f = a + u W2, fp32).  LayerNorm stays a row pass
+(csrc/svd_layer.cu): its statistics span a whole row of D columns, wider
+than an output tile.  The residual stream x stays fp32 like the reference's
+float32 latent.
 """
 
 from __future__ import annotations
@@ -139,6 +144,30 @@ def _as_latent(torch, x, dev):
     return t, was_numpy
 
 
+# svd_gemm epilogues (include/svdit_b200.h)
+EPI_BF16, EPI_ROPE, EPI_GELU, EPI_F32_RESID, EPI_F32 = range(5)
+
+
+def _gemm(torch, a, b, out, epilogue: int, resid=None, rope=None, rope_cols: int = 0, head_dim: int = 0,
+          n_tokens: int = 0):
+    """out = epilogue(a @ b) on the tensor cores (svd_gemm): a [M, K] and b
+    [K, N] bf16 row-major, out [M, N] bf16 or fp32 (row-major, unit column
+    stride)."""
+    M, K = a.shape
+    N = b.shape[1]
+    for name, t_ in (("a", a), ("b", b), ("out", out)):
+        if t_.stride(-1) != 1:
+            raise ShapeError(f"gemm: {name} needs a unit column stride")
+    nat.check(nat.lib().svd_gemm(
+        nat.c_void_p(a.data_ptr()), a.stride(0), nat.c_void_p(b.data_ptr()), b.stride(0),
+        nat.c_void_p(out.data_ptr()), out.stride(0), M, N, K, int(epilogue),
+        nat.c_void_p(resid.data_ptr()) if resid is not None else None,
+        resid.stride(0) if resid is not None else 0,
+        nat.c_void_p(rope.data_ptr()) if rope is not None else None, int(rope_cols), int(head_dim),
+        int(n_tokens), _stream(torch, a.device)))
+    return out
+
+
 def _qkv(dm: DeviceModel, l: int, x):
     torch = _torch()
     w = dm.layer(l)
@@ -151,10 +180,10 @@ def _qkv(dm: DeviceModel, l: int, x):
     h = torch.empty((rows, D), dtype=torch.bfloat16, device=dev)
     nat.check(nat.lib().svd_layernorm(nat.c_void_p(x.data_ptr()), None, None, nat.c_void_p(h.data_ptr()),
                                       rows, D, LN_EPS, _stream(torch, dev)))
-    qkv = torch.mm(h, w.wqkv)  # [B*N, 3D] bf16, fp32 accumulation
     table = _rope_table(torch, dev, N, d)
-    nat.check(nat.lib().svd_rope_apply(nat.c_void_p(qkv.data_ptr()), rows, 3 * D, D, N, H, d,
-                                       nat.c_void_p(table.data_ptr()), _stream(torch, dev)))
+    qkv = torch.empty((rows, 3 * D), dtype=torch.bfloat16, device=dev)
+    # [B*N, 3D] = h Wqkv with RoPE on the q and k blocks (columns [0, 2D)) in the epilogue
+    _gemm(torch, h, w.wqkv, qkv, EPI_ROPE, rope=table, rope_cols=2 * D, head_dim=d, n_tokens=N)
     view = qkv.view(B, N, 3, H, d)
     q, k, v = (view[:, :, i].permute(0, 2, 1, 3) for i in range(3))  # [B, H, N, d] strided views
     for head, code in w.planted_q.items():
@@ -162,13 +191,6 @@ def _qkv(dm: DeviceModel, l: int, x):
     for head, code in w.planted_k.items():
         k[:, head].copy_(code.expand(B, N, d))
     return q, k, v
-
-
-def _mm_f32(torch, a, b):
-    try:
-        return torch.mm(a, b, out_dtype=torch.float32)
-    except (TypeError, RuntimeError):  # older torch: bf16 result widened
-        return torch.mm(a, b).float()
 
 
 def _finish(dm: DeviceModel, l: int, x, attn):
@@ -181,17 +203,18 @@ def _finish(dm: DeviceModel, l: int, x, attn):
         raise ShapeError(f"attention output has shape {tuple(attn.shape)}, expected {(B, H, N, d)}")
     merged = attn.to(dev, torch.bfloat16).permute(0, 2, 1, 3)  # [B, N, H, d]: free when O was stored so
     merged = merged.reshape(B * N, D)
-    proj = _mm_f32(torch, merged, w.wo)
+    if merged.data_ptr() % 16 or merged.stride(0) % 8:
+        merged = merged.contiguous()
+    x2 = x.view(B * N, D)
     a = torch.empty((B * N, D), dtype=torch.float32, device=dev)
+    _gemm(torch, merged, w.wo, a, EPI_F32_RESID, resid=x2)  # a = x + O Wo
     h2 = torch.empty((B * N, D), dtype=torch.bfloat16, device=dev)
-    nat.check(nat.lib().svd_layernorm(nat.c_void_p(x.data_ptr()), nat.c_void_p(proj.data_ptr()),
-                                      nat.c_void_p(a.data_ptr()), nat.c_void_p(h2.data_ptr()), B * N, D,
-                                      LN_EPS, _stream(torch, dev)))
-    del proj
-    u = torch.mm(h2, w.w1)  # [B*N, 4D] bf16
-    nat.check(nat.lib().svd_gelu(nat.c_void_p(u.data_ptr()), u.numel(), _stream(torch, dev)))
-    f = _mm_f32(torch, u, w.w2)
-    f += a
+    nat.check(nat.lib().svd_layernorm(nat.c_void_p(a.data_ptr()), None, None, nat.c_void_p(h2.data_ptr()),
+                                      B * N, D, LN_EPS, _stream(torch, dev)))
+    u = torch.empty((B * N, w.w1.shape[1]), dtype=torch.bfloat16, device=dev)
+    _gemm(torch, h2, w.w1, u, EPI_GELU)  # GELU(h2 W1)
+    f = torch.empty((B * N, D), dtype=torch.float32, device=dev)
+    _gemm(torch, u, w.w2, f, EPI_F32_RESID, resid=a)  # f = a + u W2
     return f.view(B, N, D)
 
 

@@ -176,7 +176,8 @@ def test_candidate_evaluator_one_launch_path_matches_first_evaluation():
         ev = CandidateEvaluator(g, S.SearchParams(lam=0.05, epsilon=1.0))
         first = ev.evaluate(q, k, v)
         again = ev.evaluate(q, k, v, stripes=first.stripes)
-        np.testing.assert_array_equal(first.mse, again.mse)
+        # identical outputs; the fp64 MSE reduction (atomics) may reorder sums
+        np.testing.assert_allclose(first.mse, again.mse, rtol=1e-12, atol=0)
         assert first.choices == again.choices
         assert torch.equal(first.selected, again.selected)
 

@@ -119,3 +119,44 @@ def test_peer_path_with_split_kv(cap):
     torch.testing.assert_close(first.float(), ref.float(), atol=1.6e-2, rtol=8e-3)
     assert torch.equal(layer(q, k, v), first)
     assert not first[:, 2].any()
+
+
+def _worker_devices(rank, world, port, path):
+    """One rank per device: the NVLink / P2P path the driver's scaling run
+    takes (CUDA IPC of a torch allocation on another device, the epilogue's
+    peer stores, the stream-ordered peer barrier)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_03065_b200.sharding import PeerShardedLayer
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        specs = [S.full_spec(), S.diagonal_spec(1), S.skip_spec(), S.multi_diagonal_spec(),
+                 S.vertical_stripe_spec(stripes=(5, 33)), S.full_spec(), S.full_spec(), S.diagonal_spec(1)]
+        gen = torch.Generator().manual_seed(7)
+        q, k, v = (torch.randn(1, len(specs), 4096, 128, generator=gen).to(torch.bfloat16).to(dev)
+                   for _ in range(3))
+        plan = S.LayerPlan.from_specs(specs, S.TokenLayout(96, 16, 250, 64))
+        ref = torch.empty_like(q)
+        plan.forward(q, k, v, ref, head_dim=128)
+        layer = PeerShardedLayer(plan, world, rank, 128, dev, tuple(q.shape))
+        oks = []
+        for _ in range(5):
+            out = layer(q, k, v)
+        torch.cuda.synchronize(dev)
+        oks.append(bool(torch.equal(out, ref)))
+        layer.check()
+        dist.barrier()
+        layer.close()
+        torch.save({"ok": oks}, f"{path}.{rank}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two CUDA devices")
+def test_peer_reassembly_across_devices(tmp_path):
+    world = min(torch.cuda.device_count(), 8)
+    mp.spawn(_worker_devices, args=(world, _port(), str(tmp_path / "d")), nprocs=world, join=True)
+    res = [torch.load(f"{tmp_path / 'd'}.{r}") for r in range(world)]
+    assert all(all(r["ok"]) for r in res), res
