@@ -62,6 +62,16 @@ constexpr uint32_t kTmemCols = 512;
 #endif
 template <int D>
 constexpr bool kPQuarters = (SVD_P_QUARTERS >> (D == 128 ? 1 : 0)) & 1;
+// Lagged quarter hand-off (bit 0: d=64, bit 1: d=128): chunk c's P store is
+// waited for (tcgen05.wait::st) only after chunk c+1's exps, when it has long
+// completed, so the hand-offs stop stalling the softmax; the PV MMA still
+// starts one 32-key quarter behind the exps and the tail after the last
+// chunk is one quarter's PV.  Implies quarters.
+#ifndef SVD_P_LAG
+#define SVD_P_LAG 0
+#endif
+template <int D>
+constexpr bool kPLag = (SVD_P_LAG >> (D == 128 ? 1 : 0)) & 1;
 // two-part P handoff (d=128): the first part ends after 32-key chunk
 // SVD_P_FIRST (0..2).  0 — PV starts after the first 32 keys, the rest follows
 // as one part: -0.5% vs even halves (1), +1% for 2
@@ -434,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tn = 0;
         (void)tn;
         auto issue_pv = [&](int x, int vs, int j) {
-          if constexpr (kPQuarters<D>) {
+          if constexpr (kPQuarters<D> || kPLag<D>) {
             // P handed over in 32-key quarters: two K=16 MMAs per quarter
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
@@ -642,6 +652,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < 4; ++c) {
       uint32_t pk[16];
       exp_chunk(s, c, nm, pk, acc);
+      if constexpr (kPLag<D>) {
+        if (c > 0) {  // chunk c-1's store completed under this chunk's exps
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(bar(C::kBarP0 + 2 * (c - 1) + x));
+        }
+        ptx::tmem_st16(tp + c * 16, pk);
+        if (SVD_SUM_ROUNDED && SVD_SUM_AFTER_ST && D == 128) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ptx::acc_bf16x2(acc[i & 3], pk[i]);
+        }
+        if (c == 3) {
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(bar(C::kBarP0 + 2 * 3 + x));
+        }
+        continue;
+      }
       ptx::tmem_st16(tp + c * 16, pk);
       if (SVD_SUM_ROUNDED && SVD_SUM_AFTER_ST && D == 128) {
 #pragma unroll

@@ -46,6 +46,42 @@ def timed(fn, reps=5):
     return a.elapsed_time(b) / reps
 
 
+def _s():
+    return S._native.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def qkv_cublas():
+    """The round-1 flow: LN, cuBLAS QKV GEMM, RoPE pass (library GEMM baseline)."""
+    nat = S._native
+    wl = dm.layer(0)
+    rows = n
+    h = torch.empty((rows, D), dtype=torch.bfloat16, device="cuda")
+    nat.check(nat.lib().svd_layernorm(nat.c_void_p(x.data_ptr()), None, None, nat.c_void_p(h.data_ptr()),
+                                      rows, D, L.LN_EPS, _s()))
+    qkv = torch.mm(h, wl.wqkv)
+    table = L._rope_table(torch, x.device, n, d)
+    nat.check(nat.lib().svd_rope_apply(nat.c_void_p(qkv.data_ptr()), rows, 3 * D, D, n, H, d,
+                                       nat.c_void_p(table.data_ptr()), _s()))
+    return qkv
+
+
+def finish_cublas(attn):
+    """The round-1 flow: cuBLAS out-proj, LN with fused residual, cuBLAS W1, GELU pass, cuBLAS W2, + a."""
+    nat = S._native
+    wl = dm.layer(0)
+    merged = attn.permute(0, 2, 1, 3).reshape(n, D)
+    proj = torch.mm(merged, wl.wo, out_dtype=torch.float32)
+    a = torch.empty((n, D), dtype=torch.float32, device="cuda")
+    h2 = torch.empty((n, D), dtype=torch.bfloat16, device="cuda")
+    nat.check(nat.lib().svd_layernorm(nat.c_void_p(x.data_ptr()), nat.c_void_p(proj.data_ptr()),
+                                      nat.c_void_p(a.data_ptr()), nat.c_void_p(h2.data_ptr()), n, D, L.LN_EPS, _s()))
+    u = torch.mm(h2, wl.w1)
+    nat.check(nat.lib().svd_gelu(nat.c_void_p(u.data_ptr()), u.numel(), _s()))
+    f = torch.mm(u, wl.w2, out_dtype=torch.float32)
+    f += a
+    return f
+
+
 q, k, v = L._qkv(dm, 0, x)
 o = torch.empty(1, n, H, d, dtype=torch.bfloat16, device="cuda")
 res = {"config": cfgname, "tokens": n, "hidden": D}
@@ -53,6 +89,16 @@ res["qkv_ms"] = timed(lambda: L._qkv(dm, 0, x))
 res["attention_ms"] = timed(lambda: S.fused_layer_attention(q, k, v, groups, out=o.permute(0, 2, 1, 3)))
 res["finish_ms"] = timed(lambda: L._finish(dm, 0, x, o.permute(0, 2, 1, 3)))
 res["layer_forward_ms"] = timed(lambda: L.layer_forward(dm, 0, x, specs))
+res["qkv_cublas_ms"] = timed(qkv_cublas)
+res["finish_cublas_ms"] = timed(lambda: finish_cublas(o.permute(0, 2, 1, 3)))
+res["gemm_part_ours_ms"] = res["qkv_ms"] + res["finish_ms"]
+res["gemm_part_cublas_ms"] = res["qkv_cublas_ms"] + res["finish_cublas_ms"]
+# agreement of the two flows (fp32 accumulation in both; RoPE rounds once in ours, twice in the library flow)
+ref = finish_cublas(o.permute(0, 2, 1, 3))
+ours = L._finish(dm, 0, x, o.permute(0, 2, 1, 3)).view(n, D)
+res["finish_max_abs_diff"] = float((ref - ours).abs().max())
+res["qkv_max_abs_diff"] = float((qkv_cublas().float() - torch.cat(
+    [t_.permute(0, 2, 1, 3).reshape(n, D).float() for t_ in L._qkv(dm, 0, x)], dim=1)).abs().max())
 res["attention_share"] = res["attention_ms"] / (res["qkv_ms"] + res["attention_ms"] + res["finish_ms"])
 res["linear_tflops"] = S.layer_linear_flops(n, D) / ((res["qkv_ms"] + res["finish_ms"]) * 1e-3) / 1e12
 print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in res.items()}))
