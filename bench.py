@@ -432,6 +432,7 @@ def _search_step(S, layout, q, k, v, stream, dev):
     H, d = q.shape[1], q.shape[-1]
     full_plan = S.plan_for_assignment([S.full_spec()] * H, layout)
     o = torch.empty_like(q)
+    full_plan.forward(q, k, v, o, head_dim=d)  # device tables uploaded outside the timed region
     ev_ = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev_[0].record(stream)
     block_key_mass(q, k, grid)
