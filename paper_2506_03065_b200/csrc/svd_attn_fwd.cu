@@ -808,6 +808,399 @@ __global__ void __launch_bounds__(kThreads, 1)
   named_bar_sync(1, 32 + 256);
 }
 
+// ---------------------------------------------------------------------------
+// d=128 half-row pair kernel (`svd_hp_kernel<FINE>`).
+//
+// The two-tile kernel above keeps S_A, S_B, O_A, O_B in the 512 TMEM columns,
+// so P_X must alias S_X and every tile step is the serial chain
+// softmax_X(j) -> PV_X(j) -> S_X(j+1) -> softmax_X(j+1): the softmax warps
+// wait for S ~36% of the time.  Here one work item (two 128-row Q tiles with
+// one KV list) runs on a cluster of two CTAs, ONE tile per CTA, and TMEM
+// holds two S buffers and two O accumulators per CTA:
+//   S[0], S[1]  double-buffered scores: S(j+1) (even S(j+2)) is computed while
+//               the softmax works on S(j)
+//   O_0, O_1    the output of key halves 0 / 1: softmax warpgroup h owns the
+//               64-key half h of every 128-key step with its own running max,
+//               row sum and O_h (no per-step exchange); the epilogue merges
+//               O = (2^(m0-M) O_0 + 2^(m1-M) O_1) / (2^(m0-M) l0 + 2^(m1-M) l1)
+// The leader CTA issues cta_group::2 MMAs (M = 256: both CTAs' tiles) whose B
+// operand is split across the pair — each CTA stages one 64-key segment of
+// K (S = Q K^T, N = 128 keys) and one 64-column half of d of V
+// (O_h += P_h V_h, N = d) — so the pair reads every K / V tile from L2 once.
+//
+// CTA (384 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer
+// (leader only), warps 4-7 / 8-11 softmax for key half 0 / 1, epilogue for
+// columns [0, 64) / [64, 128) of d.
+namespace hp {
+constexpr int kQBytes = 128 * 128 * 2;   // this CTA's Q tile: 2 slabs x 128 rows x 128 B
+constexpr int kQSlab = 128 * 128;
+constexpr int kKStage = 64 * 128 * 2;    // one 64-key segment, all of d (2 slabs x 64 rows)
+constexpr int kKSlab = 64 * 128;
+constexpr int kVStage = 128 * 64 * 2;    // 128 keys, this CTA's 64 columns of d
+constexpr int kKSt = 5, kVSt = 5;
+constexpr int kOffQ = 0;
+constexpr int kOffK = kOffQ + kQBytes;
+constexpr int kOffV = kOffK + kKSt * kKStage;
+constexpr int kOffBar = kOffV + kVSt * kVStage;
+// barriers: q | kfull kempty | vfull vempty | s_full[2] | p[2 bufs][2 halves] | pv_done[2] | o_full
+constexpr int kBarQ = 0;
+constexpr int kBarKF = 1, kBarKE = kBarKF + kKSt;
+constexpr int kBarVF = kBarKE + kKSt, kBarVE = kBarVF + kVSt;
+constexpr int kBarSF = kBarVE + kVSt;
+constexpr int kBarP = kBarSF + 2;   // + 2 * buf + h (leader's; both CTAs' warps arrive)
+constexpr int kBarPD = kBarP + 4;   // + h: PV_h(j) complete (O_h final through step j)
+constexpr int kBarO = kBarPD + 2;
+constexpr int kNumBars = kBarO + 1;
+constexpr int kOffSlot = kOffBar + kNumBars * 8;
+constexpr int kOffXch = (kOffSlot + 16 + 15) & ~15;  // (m, l) per [half][row]
+constexpr int kSmemBytes = kOffXch + 2 * 2 * 128 * 4 + 1024;
+__device__ constexpr uint32_t col_s(int buf) { return buf ? 128u : 0u; }
+__device__ constexpr uint32_t col_o(int h) { return h ? 384u : 256u; }
+}  // namespace hp
+
+#ifndef SVD_HP_EMU
+#define SVD_HP_EMU 3
+#endif
+
+
+template <bool FINE>
+__global__ void __launch_bounds__(kThreads, 1)
+    svd_hp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* base_ptr = smem_raw + (base - raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  auto bar = [&](int i) { return base + hp::kOffBar + 8u * uint32_t(i); };
+  const int rank = int(ptx::cluster_ctarank());  // = the Q tile of the item this CTA holds
+  const bool leader = rank == 0;
+  const WorkItem* itp = p.items + (blockIdx.x >> 1);
+  const int b = blockIdx.y;
+  const int n_kv = itp->kv_count;
+  const int head = itp->head;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(bar(hp::kBarQ), 1);
+    for (int i = 0; i < hp::kKSt; ++i) {
+      ptx::mbar_init(bar(hp::kBarKF + i), 1);
+      ptx::mbar_init(bar(hp::kBarKE + i), 1);
+    }
+    for (int i = 0; i < hp::kVSt; ++i) {
+      ptx::mbar_init(bar(hp::kBarVF + i), 1);
+      ptx::mbar_init(bar(hp::kBarVE + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(bar(hp::kBarSF + i), 1);
+      ptx::mbar_init(bar(hp::kBarPD + i), 1);
+    }
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(bar(hp::kBarP + i), 2 * 4);  // 4 warps x 2 CTAs
+    ptx::mbar_init(bar(hp::kBarO), 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc_cg2(base + hp::kOffSlot, kTmemCols);
+    ptx::tmem_relinquish_cg2();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();  // the peer's barriers and TMEM exist
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(base_ptr + hp::kOffSlot);
+  auto pair_exit = [&]() {
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // the leader's MMAs into this CTA's TMEM and all remote arrivals are done
+    if (warp == 1) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc_cg2(tmem, kTmemCols);
+    }
+  };
+
+  if (warp < 4) {
+    ptx::reg_dealloc<SVD_REG_LOW>();
+    if (warp == 0 && lane == 0 && n_kv > 0) {
+      // ---------------------------------------------------------- TMA producer (both CTAs)
+      ptx::prefetch_tmap(&tm_q);
+      ptx::prefetch_tmap(&tm_k);
+      ptx::prefetch_tmap(&tm_v);
+      const uint64_t pol_q = ptx::policy_evict_first();
+      const uint64_t pol_kv = ptx::policy_evict_last();
+      const int in_head = p.in_head_map ? __ldg(p.in_head_map + head) : head;
+      const int first = itp->qseg[0];
+      if (leader) ptx::mbar_arrive_expect_tx(bar(hp::kBarQ), 2 * hp::kQBytes);
+      const uint32_t qbar = ptx::mapa_shared(bar(hp::kBarQ), 0);
+#pragma unroll
+      for (int slot = 0; slot < 2; ++slot) {
+        const int sg = itp->qseg[2 * rank + slot];
+        const int seg = sg >= 0 ? sg : first;
+#pragma unroll
+        for (int slab = 0; slab < 2; ++slab)
+          ptx::tma_load_4d_cg2(base + hp::kOffQ + slab * hp::kQSlab + slot * (64 * 128), &tm_q, qbar, slab * 64,
+                               seg * kSeg, in_head, b, pol_q);
+      }
+      const KvEntry* kvp = p.kv + itp->kv_begin;
+      for (int j = 0; j < n_kv; ++j) {
+        const KvEntry e = load_kv(kvp + j);
+        const int k0 = e.kseg0, k1 = e.kseg1 >= 0 ? e.kseg1 : e.kseg0;
+        const int ks = j % hp::kKSt, vs = j % hp::kVSt;
+        // K: this CTA's 64-key segment (the B rows its half of the S MMA reads)
+        ptx::mbar_wait(bar(hp::kBarKE + ks), ((j / hp::kKSt) & 1) ^ 1);
+        if (leader) ptx::mbar_arrive_expect_tx(bar(hp::kBarKF + ks), 2 * hp::kKStage);
+        const uint32_t kbar = ptx::mapa_shared(bar(hp::kBarKF + ks), 0);
+        const int kseg = rank ? k1 : k0;
+#pragma unroll
+        for (int slab = 0; slab < 2; ++slab)
+          ptx::tma_load_4d_cg2(base + hp::kOffK + ks * hp::kKStage + slab * hp::kKSlab, &tm_k, kbar, slab * 64,
+                               kseg * kSeg, in_head, b, pol_kv);
+        // V: both segments, this CTA's 64 columns of d
+        ptx::mbar_wait(bar(hp::kBarVE + vs), ((j / hp::kVSt) & 1) ^ 1);
+        if (leader) ptx::mbar_arrive_expect_tx(bar(hp::kBarVF + vs), 2 * hp::kVStage);
+        const uint32_t vbar = ptx::mapa_shared(bar(hp::kBarVF + vs), 0);
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot)
+          ptx::tma_load_4d_cg2(base + hp::kOffV + vs * hp::kVStage + slot * (64 * 128), &tm_v, vbar, rank * 64,
+                               (slot ? k1 : k0) * kSeg, in_head, b, pol_kv);
+      }
+    }
+    if (warp == 1 && leader && n_kv > 0) {
+      // ---------------------------------------------------------- MMA issuer (leader)
+      uint32_t sb = base, tb = tmem;
+      constexpr uint32_t id_s = ptx::idesc_bf16(256, 128, false);
+      constexpr uint32_t id_pv = ptx::idesc_bf16(256, 128, true);
+      constexpr uint32_t hi = ptx::sw128_hi(1024);
+      constexpr uint16_t kBoth = 0x3;
+      auto issue_s = [&](int buf, int ks) {
+        const uint32_t qlo = ptx::sw128_lo(sb + hp::kOffQ, 16);
+        const uint32_t klo = ptx::sw128_lo(sb + hp::kOffK + ks * hp::kKStage, 16);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t qoff = ((kk >> 2) * hp::kQSlab + (kk & 3) * 32) >> 4;
+          const uint32_t koff = ((kk >> 2) * hp::kKSlab + (kk & 3) * 32) >> 4;
+          ptx::mma_ss_cg2_e(tb + hp::col_s(buf), qlo + qoff, hi, klo + koff, hi, id_s, kk > 0);
+        }
+      };
+      ptx::mbar_wait(bar(hp::kBarQ), 0);
+      ptx::mbar_wait(bar(hp::kBarKF + 0), 0);
+      ptx::tc_fence_after();
+      issue_s(0, 0);
+      ptx::mma_commit_cg2_mc_e(bar(hp::kBarSF + 0), kBoth);
+      ptx::mma_commit_cg2_mc_e(bar(hp::kBarKE + 0), kBoth);
+      if (n_kv > 1) {
+        ptx::mbar_wait(bar(hp::kBarKF + 1 % hp::kKSt), 0);
+        ptx::tc_fence_after();
+        issue_s(1, 1 % hp::kKSt);
+        ptx::mma_commit_cg2_mc_e(bar(hp::kBarSF + 1), kBoth);
+        ptx::mma_commit_cg2_mc_e(bar(hp::kBarKE + 1 % hp::kKSt), kBoth);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        asm volatile("" : "+r"(sb), "+r"(tb));
+        const int buf = j & 1;
+        const int vs = j % hp::kVSt;
+        ptx::mbar_wait(bar(hp::kBarVF + vs), (j / hp::kVSt) & 1);
+        const uint32_t vlo = ptx::sw128_lo(sb + hp::kOffV + vs * hp::kVStage, hp::kVStage);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          // O_h += P_h(j) V_h(j): keys [64h, 64h + 64) of the step
+          ptx::mbar_wait(bar(hp::kBarP + 2 * buf + h), (j >> 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::mma_ts_cg2_e(tb + hp::col_o(h), tb + hp::col_s(buf) + 64 * h + kk * 8,
+                              vlo + ((h * 8192 + kk * 2048) >> 4), hi, id_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          ptx::mma_commit_cg2_mc_e(bar(hp::kBarPD + h), kBoth);
+        }
+        ptx::mma_commit_cg2_mc_e(bar(hp::kBarVE + vs), kBoth);
+        if (j + 2 < n_kv) {
+          // S(j+2) into the buffer P(j) occupied: the in-order tensor pipe
+          // runs it after both PV halves have read P(j)
+          const int ks = (j + 2) % hp::kKSt;
+          ptx::mbar_wait(bar(hp::kBarKF + ks), ((j + 2) / hp::kKSt) & 1);
+          ptx::tc_fence_after();
+          issue_s(buf, ks);
+          ptx::mma_commit_cg2_mc_e(bar(hp::kBarSF + buf), kBoth);
+          ptx::mma_commit_cg2_mc_e(bar(hp::kBarKE + ks), kBoth);
+        }
+      }
+      ptx::mma_commit_cg2_mc_e(bar(hp::kBarO), kBoth);
+    }
+    __syncwarp();
+    pair_exit();
+    return;
+  }
+
+  // -------------------------------------------------------------- softmax (key half h) / epilogue
+  ptx::reg_alloc<SVD_REG_HIGH>();
+  const int h = (warp - 4) >> 2;
+  const int wq = warp & 3;
+  const int row = wq * 32 + lane;
+  const uint32_t lane_off = uint32_t(wq * 32) << 16;
+  const int x = rank;
+  const int qslot = 2 * x + (row >> 6);
+  const int qseg = itp->qseg[qslot];
+  const int tok_r = qseg * kSeg + (row & 63);
+  const bool row_valid = qseg >= 0 && tok_r < p.n_tokens;
+  int64_t orow;
+  if (p.packed && p.n_peers == 0)
+    orow = (int64_t(itp->out_base) + qslot * kSeg + (row & 63)) * p.o_sn;
+  else
+    orow = int64_t(b) * p.o_sb + int64_t(p.o_head_map ? __ldg(p.o_head_map + head) : head) * p.o_sh +
+           int64_t(tok_r) * p.o_sn;
+  orow += 64 * h;  // this warpgroup's 64 columns of d
+  if (n_kv == 0) {
+    // SKIP head (attention.py:51-54): exact zeros
+    if (row_valid) {
+      const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) store_row16(p, orow + c * 8, z);
+    }
+    pair_exit();
+    return;
+  }
+  const uint32_t* bits_row = nullptr;
+  if constexpr (FINE) {
+    const int qb = min(max(tok_r, 0) / p.block_size, p.n_blocks - 1);
+    bits_row = p.bits + p.bit_off[itp->group] + int64_t(qb) * p.words_per_row;
+  }
+  const float sl2 = p.scale_log2;
+  const float2 sl2x2 = make_float2(sl2, sl2);
+  float m = -INFINITY;  // this half's running max (log2 domain), lazily updated
+  float l = 0.f;        // this half's running denominator relative to m
+  const KvEntry* kvp = p.kv + itp->kv_begin;
+  KvEntry e_next = load_kv(kvp);
+  const uint32_t to = tmem + lane_off + hp::col_o(h);
+  const uint32_t p_arrive = ptx::mapa_shared(bar(hp::kBarP), 0);  // the leader's P barriers
+  for (int j = 0; j < n_kv; ++j) {
+    const KvEntry e = e_next;
+    if (j + 1 < n_kv) e_next = load_kv(kvp + j + 1);
+    const int buf = j & 1;
+    const uint32_t ts = tmem + lane_off + hp::col_s(buf) + 64u * uint32_t(h);
+    ptx::mbar_wait(bar(hp::kBarSF + buf), (j >> 1) & 1);
+    ptx::tc_fence_after();
+    float s[64];
+    ptx::tmem_ld32(ts + 0, *reinterpret_cast<float(*)[32]>(&s[0]));
+    ptx::tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+    ptx::tmem_wait_ld();
+    if (!(e.flags & kFlagAll)) {
+      const int kseg = h ? e.kseg1 : e.kseg0;
+      const bool on = ((e.flags >> (2 * qslot + h)) & 1u) && kseg >= 0;
+      const int lim = on ? min(kSeg, p.n_tokens - kseg * kSeg) : 0;
+      if constexpr (FINE) {
+        const uint64_t mk = fine_segment_mask(kseg, lim, p, bits_row);
+        const uint32_t w0 = uint32_t(mk), w1 = uint32_t(mk >> 32);
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (!((((i < 32) ? w0 : w1) >> (i & 31)) & 1u)) s[i] = -INFINITY;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= lim) s[i] = -INFINITY;
+      }
+    }
+    float mp[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) mp[t] = fmaxf(s[t], s[8 + t]);
+#pragma unroll
+    for (int i = 16; i < 64; i += 16)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mp[t] = fmaxf(mp[t], fmaxf(s[i + t], s[i + 8 + t]));
+    const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                           fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+    const float m_new = fmaxf(m, mx * sl2);
+    const bool resc = m_new > m + 8.0f;  // lazy rescale: keep a stale max unless it grew by > 2^8
+    if (__any_sync(0xffffffffu, resc)) {
+      const float alpha = resc ? ptx::ex2(m - m_new) : 1.0f;
+      if (j > 0) {
+        // O_h is final through step j-1 once PV_h(j-1) completes
+        ptx::mbar_wait(bar(hp::kBarPD + h), (j - 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float ov[16];
+          ptx::tmem_ld16(to + c * 16, ov);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ov[i] *= alpha;
+          ptx::tmem_st16(to + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(ov));
+        }
+      }
+      if (resc) {
+        l *= alpha;
+        m = m_new;
+      }
+    }
+    const float mref = (m == -INFINITY) ? 0.f : m;
+    const float2 nm = make_float2(-mref, -mref);
+    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                     make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 xv = ptx::ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sl2x2, nm);
+        float2 pv;
+        if (SVD_HP_EMU > 0 && (i & 7) < SVD_HP_EMU) {
+          pv = ptx::ex2_poly2_deg2(xv);
+        } else {
+          pv.x = ptx::ex2(xv.x);
+          pv.y = ptx::ex2(xv.y);
+        }
+        pk[i] = ptx::pack_bf16(pv.x, pv.y);
+        ptx::acc_bf16x2(acc[i & 3], pk[i]);
+      }
+      // P_h of keys [32c, 32c + 32) of this half -> columns [16c, 16c + 16)
+      // of the half's (already loaded) S columns
+      ptx::tmem_st16(ts + c * 16, pk);
+    }
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_remote(p_arrive + 8u * uint32_t(2 * buf + h));
+    const float2 a = ptx::fadd2(ptx::fadd2(acc[0], acc[1]), ptx::fadd2(acc[2], acc[3]));
+    l += a.x + a.y;
+  }
+
+  // epilogue: merge the halves' (m, l, O_h); this warpgroup writes d columns [64h, 64h + 64)
+  ptx::mbar_wait(bar(hp::kBarO), 0);
+  ptx::tc_fence_after();
+  float* xch = reinterpret_cast<float*>(base_ptr + hp::kOffXch);  // [h][m|l][128]
+  xch[(h * 2 + 0) * 128 + row] = m;
+  xch[(h * 2 + 1) * 128 + row] = l;
+  named_bar_sync(2, 256);
+  const float m_o = xch[((1 - h) * 2 + 0) * 128 + row], l_o = xch[((1 - h) * 2 + 1) * 128 + row];
+  const float M = fmaxf(m, m_o);
+  const float w_me = m == -INFINITY ? 0.f : ptx::ex2(m - M);
+  const float w_ot = m_o == -INFINITY ? 0.f : ptx::ex2(m_o - M);
+  const float L = w_me * l + w_ot * l_o;
+  const float inv = L > 0.f ? 1.0f / L : 0.f;
+  const float w0 = (h == 0 ? w_me : w_ot) * inv, w1 = (h == 0 ? w_ot : w_me) * inv;
+  float chk = L * 0.f;  // NaN once any accumulator (or L) is Inf / NaN
+  const uint32_t o0 = tmem + lane_off + hp::col_o(0) + 64u * uint32_t(h);
+  const uint32_t o1 = tmem + lane_off + hp::col_o(1) + 64u * uint32_t(h);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float a0[16], a1[16];
+    ptx::tmem_ld16(o0 + c * 16, a0);
+    ptx::tmem_ld16(o1 + c * 16, a1);
+    ptx::tmem_wait_ld();
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      pk[i] = ptx::pack_bf16(a0[2 * i] * w0 + a1[2 * i] * w1, a0[2 * i + 1] * w0 + a1[2 * i + 1] * w1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) chk = fmaf(a0[i] + a1[i], 0.f, chk);
+    if (row_valid) {
+      store_row16(p, orow + c * 16, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+      store_row16(p, orow + c * 16 + 8, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+    }
+  }
+  if (p.nonfinite && row_valid && chk != 0.f) atomicOr(p.nonfinite, 1);
+  if (h == 0 && qseg >= 0) store_row_stats(p, b, head, tok_r, row_valid, M, L);
+  if (p.n_peers > 0) __threadfence_system();
+  pair_exit();
+}
+
 // Stream-ordered barrier over peer memory (multi-GPU step boundary without a
 // host sync): thread r publishes `epoch` into slot `rank` of rank r's flag
 // array (release, system scope), then thread r waits until slot r of this
@@ -987,6 +1380,32 @@ void release_device_tables(const svd_plan* P) {
   cudaSetDevice(cur);
 }
 
+// d=128 half-row pair kernel only with SVD_HP=1: correct (the GPU suite runs
+// it) and free of the per-tile S wait, but measured 2-3% slower than the
+// two-tile kernel (profiles/r2/KERNEL_NOTES_r2.md)
+static bool use_hp() {
+  const char* v = std::getenv("SVD_HP");
+  return v && std::strcmp(v, "1") == 0;
+}
+
+template <bool FINE>
+static cudaError_t launch_hp(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                             const FwdParams& prm, int64_t n_items, int batch, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(unsigned(2 * n_items), unsigned(batch));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = hp::kSmemBytes;
+  cfg.stream = stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, svd_hp_kernel<FINE>, mq, mk, mv, prm);
+}
+
 template <int D>
 static int launch_fwd(const svd_plan* P, DeviceTables* T, const svd_fwd_args& a, cudaStream_t stream,
                       void* const* peers = nullptr, int n_peers = 0) {
@@ -1044,6 +1463,21 @@ static int launch_fwd(const svd_plan* P, DeviceTables* T, const svd_fwd_args& a,
   }
   for (int r = 0; r < n_peers; ++r) prm.peer_o[r] = static_cast<__nv_bfloat16*>(peers[r]);
   if (T->n_items == 0) return SVD_OK;
+  if (D == 128 && P->n_split_groups == 0 && use_hp()) {
+    static bool hp_attr[64] = {false};
+    if (dev < 64 && !hp_attr[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(svd_hp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           hp::kSmemBytes);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(svd_hp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp::kSmemBytes);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute (half-row pair kernel)");
+      hp_attr[dev] = true;
+    }
+    cudaError_t e = P->fine ? launch_hp<true>(mq, mk, mv, prm, T->n_items, batch, stream)
+                            : launch_hp<false>(mq, mk, mv, prm, T->n_items, batch, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svd_hp_kernel launch");
+    return SVD_OK;
+  }
   dim3 grid(unsigned(T->n_items), unsigned(batch));
   if (P->fine) {
     svd_fwd_kernel<D, true><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);

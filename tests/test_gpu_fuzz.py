@@ -50,9 +50,14 @@ def _random_case(rng):
     return lay, specs, d, B, qscale
 
 
-@pytest.mark.parametrize("seed", [4, 2])
-def test_random_layers_vs_oracle(seed):
+@pytest.mark.parametrize("seed,kernel", [(4, "default"), (2, "default"), (3, "hp")])
+def test_random_layers_vs_oracle(seed, kernel, monkeypatch):
+    """kernel "hp": d=128 layers run the opt-in half-row CTA-pair kernel
+    (SVD_HP=1, csrc/svd_attn_fwd.cu svd_hp_kernel); d <= 64 the usual one."""
     import torch
+
+    if kernel == "hp":
+        monkeypatch.setenv("SVD_HP", "1")
 
     rng = np.random.default_rng(1234 + seed)
     worst = 0.0

@@ -168,10 +168,15 @@ def test_ones_probe_and_partition_probe_full_size():
     assert out[..., 2:].abs().max().item() == 0.0
 
 
-def test_full_size_sampled_rows_vs_oracle():
+@pytest.mark.parametrize("kernel", ["default", "hp"])
+def test_full_size_sampled_rows_vs_oracle(kernel, monkeypatch):
     """HunyuanVideo layout at full N: sampled query blocks (incl. text/forced
-    rows and the partial tail) of a diagonal, a multi-diagonal and a FULL head."""
+    rows and the partial tail) of a diagonal, a multi-diagonal and a FULL head
+    (kernel "hp": the opt-in half-row CTA-pair kernel, SVD_HP=1)."""
     import torch
+
+    if kernel == "hp":
+        monkeypatch.setenv("SVD_HP", "1")
 
     lay = (256, 33, 3600, 64)
     og = O.block_grid(*lay)
