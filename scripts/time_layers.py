@@ -27,7 +27,7 @@ for c in configs:
         plan.forward(q, k, v, out, head_dim=d)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 3 if dense else 8
+    reps = int(os.environ.get("REPS", 3 if dense else 8))
     a.record()
     for _ in range(reps):
         plan.forward(q, k, v, out, head_dim=d)
