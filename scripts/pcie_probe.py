@@ -11,7 +11,9 @@ x2 = torch.empty(n, dtype=torch.bfloat16).pin_memory()
 y2 = torch.empty(n, dtype=torch.bfloat16, device="cuda")
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 res = {}
-for name in ("h2d", "d2h", "both"):
+s3 = torch.cuda.Stream()
+half = n // 2
+for name in ("h2d", "d2h", "both", "h2d_2streams", "h2d_8chunks"):
     ts = []
     for _ in range(4):
         torch.cuda.synchronize()
@@ -22,6 +24,16 @@ for name in ("h2d", "d2h", "both"):
         if name in ("d2h", "both"):
             with torch.cuda.stream(s2):
                 x2.copy_(y2, non_blocking=True)
+        if name == "h2d_2streams":  # two halves on two streams at once (two copy engines?)
+            with torch.cuda.stream(s1):
+                y[:half].copy_(x[:half], non_blocking=True)
+            with torch.cuda.stream(s3):
+                y[half:].copy_(x[half:], non_blocking=True)
+        if name == "h2d_8chunks":  # the host pipeline's granularity: 8 copies in a row
+            with torch.cuda.stream(s1):
+                for c in range(8):
+                    sl = slice(c * n // 8, (c + 1) * n // 8)
+                    y[sl].copy_(x[sl], non_blocking=True)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     res[name + "_GBps"] = round(n * 2 / min(ts) / 1e9, 1)
