@@ -170,6 +170,11 @@ int svd_plan_shard_ex(const svd_plan* plan, int32_t world, int32_t rank, int32_t
                       int32_t max_item_tiles, int32_t partition, svd_plan** shard);
 int svd_plan_shard_rows(const svd_plan* shard, int64_t* n_rows, int32_t* row_head,
                         int32_t* row_token);
+/* The work items of a shard plan that belong to the listed heads, as a shard
+ * plan with the parent's packed row layout (one chunk of a rank's pipelined
+ * end-to-end step: copy-in of a head chunk overlaps the previous chunk's
+ * kernel).  No reference counterpart (multi-GPU is this repo's own). */
+int svd_plan_shard_heads(const svd_plan* shard, const int32_t* heads, int32_t n_heads, svd_plan** out);
 
 /* Kernel schedule dump (tests / tooling): items as 12 int32 each
  * {head, group, kv_begin, kv_count, qseg[4], out_base, 0, 0, 0} and KV

@@ -116,6 +116,7 @@ SIGNATURES = {
     "svd_plan_shard_sm": (c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, POINTER(c_void_p)]),
     "svd_plan_shard_ex": (c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, POINTER(c_void_p)]),
     "svd_plan_shard_rows": (c_int, [c_void_p, POINTER(c_int64), c_void_p, c_void_p]),
+    "svd_plan_shard_heads": (c_int, [c_void_p, c_void_p, c_int32, POINTER(c_void_p)]),
     "svd_attn_fwd": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -177,6 +177,14 @@ class LayerPlan:
                                               nat.ctypes.byref(out)))
         return LayerPlan(out.value, self.layout, self.n_heads, sharded=True)
 
+    def shard_subset(self, heads) -> "LayerPlan":
+        """The items of this shard plan that belong to `heads` (a shard plan
+        with the same packed row layout): one chunk of a pipelined step."""
+        arr = np.ascontiguousarray(np.asarray(heads, dtype=np.int32))
+        out = nat.c_void_p()
+        nat.check(nat.lib().svd_plan_shard_heads(self._handle, nat.ptr(arr), int(arr.size), nat.ctypes.byref(out)))
+        return LayerPlan(out.value, self.layout, self.n_heads, sharded=True)
+
     def shard_heads(self) -> tuple[int, ...]:
         """Heads this shard's items touch (ascending)."""
         items, _ = self.schedule()

@@ -922,6 +922,45 @@ int svd_plan_shard(const svd_plan* P, int32_t world, int32_t rank, svd_plan** sh
   return svd_plan_shard_sm(P, world, rank, 148, 0, shard);
 }
 
+// The items of a shard plan that belong to the listed heads (split-KV parts
+// included: they share their head), as a shard plan with the parent's packed
+// row layout — one chunk of a rank's pipelined end-to-end step.
+int svd_plan_shard_heads(const svd_plan* S, const int32_t* heads, int32_t n_heads, svd_plan** out) {
+  if (!S || !heads || !out) return fail(SVD_ERR_CONFIG, "NULL argument");
+  *out = nullptr;
+  if (!S->sharded) return fail(SVD_ERR_CONFIG, "not a shard plan");
+  if (n_heads < 1) return fail(SVD_ERR_CONFIG, "need at least one head");
+  std::vector<uint8_t> keep(size_t(S->n_heads), 0);
+  for (int32_t i = 0; i < n_heads; ++i) {
+    if (heads[i] < 0 || heads[i] >= S->n_heads) return fail(SVD_ERR_CONFIG, "head out of range");
+    if (keep[size_t(heads[i])]++) return fail(SVD_ERR_CONFIG, "duplicate head");
+  }
+  auto* C = new svd_plan();
+  C->layout = S->layout;
+  C->grid = S->grid;
+  C->nseg = S->nseg;
+  C->n_heads = S->n_heads;
+  C->fine = S->fine;
+  C->cluster = S->cluster;
+  C->head_group = S->head_group;
+  C->groups = S->groups;
+  C->kv = S->kv;
+  C->fine_bits = S->fine_bits;
+  C->fine_bit_off = S->fine_bit_off;
+  C->active_pairs = S->active_pairs;
+  C->sharded = true;
+  C->n_split_groups = S->n_split_groups;  // group ids kept: scratch sized as the parent's
+  C->max_split_parts = S->max_split_parts;
+  C->n_rows = S->n_rows;
+  C->row_head = S->row_head;
+  C->row_token = S->row_token;
+  for (const auto& it : S->items)
+    if (keep[size_t(it.head)]) C->items.push_back(it);
+  for (const auto& it : C->items) C->computed_tiles += 2 * int64_t(it.kv_count);
+  *out = C;
+  return SVD_OK;
+}
+
 int svd_plan_shard_rows(const svd_plan* S, int64_t* n_rows, int32_t* row_head, int32_t* row_token) {
   if (!S || !S->sharded) return fail(SVD_ERR_CONFIG, "not a shard plan");
   if (n_rows) *n_rows = S->n_rows;

@@ -20,6 +20,9 @@ import numpy as np
 from . import _native as nat
 from .attention import LayerPlan
 
+# head chunks of a rank's pipelined end-to-end step (PeerShardedLayer.e2e)
+E2E_CHUNKS = int(__import__("os").environ.get("SVD_E2E_CHUNKS", "3"))
+
 
 def gathered_row_maps(plan: LayerPlan, world: int, max_item_tiles: int = 0):
     """(shards, row_head, row_token, max_rows) for the all-gathered buffer:
@@ -155,22 +158,96 @@ class PeerShardedLayer:
         if int(self.timed_out.item()) != 0:
             raise nat.NativeError("peer barrier timed out: a rank did not finish its step")
 
+    def _e2e_plan(self, n_tokens: int):
+        """(chunks, owned) for the pipelined end-to-end step: this rank's heads
+        in up to E2E_CHUNKS chunks of about equal copy-in bytes, the
+        kernel-heaviest first (the first kernel starts early, the light heads'
+        copies hide under the heavy heads' kernels), each with its sub-plan;
+        and the heads whose rows this rank computes all of (their D2H can
+        leave right after their chunk's kernel — a boundary head shared with
+        a neighbour waits for the step barrier)."""
+        cached = self.__dict__.get("_e2e_cache")
+        if cached is not None and cached[0] == n_tokens:
+            return cached[1], cached[2]
+        items, _ = self.shard.schedule()
+        cost = {h: 0.0 for h in self.heads}
+        for it in items:
+            cost[int(it[0])] = cost.get(int(it[0]), 0.0) + float(it[3]) + 4.0
+        order = sorted(self.heads, key=lambda h: (-cost[h], h))
+        k = max(1, min(E2E_CHUNKS, len(order)))
+        bounds = [round(i * len(order) / k) for i in range(k + 1)]
+        chunks = []
+        for c in range(k):
+            hs = tuple(order[bounds[c]:bounds[c + 1]])
+            sub = self.shard.shard_subset(hs) if self.shard.sharded else self.shard.heads_subplan(hs)
+            chunks.append((hs, sub))
+        if self.world == 1 or not self.shard.sharded:
+            owned = set(self.heads)
+        else:
+            rh, rt = self.shard.shard_rows()
+            valid = rt >= 0
+            counts = np.bincount(rh[valid], minlength=self.plan.n_heads)
+            owned = {h for h in self.heads if counts[h] == n_tokens}
+        self._e2e_cache = (n_tokens, chunks, owned)
+        return chunks, owned
+
     def e2e(self, hq, hk, hv, hout, groups=None):
-        """End-to-end step from pinned host buffers: H2D of the heads this
-        rank reads, the fused shard kernel (rows land in every rank's O) and
-        the step barrier, D2H of those heads of O (the ranks' head sets cover
-        every head)."""
+        """End-to-end step from pinned host buffers, pipelined per head chunk:
+        H2D of chunk c (copy stream) overlaps the shard kernel of chunk c-1
+        (the caller's stream; rows land in every rank's O), the D2H of the
+        heads this rank fully computes follows each chunk's kernel on a third
+        stream, the boundary heads' D2H follows the stream-ordered step
+        barrier.  Returns once hout holds this rank's heads."""
         import torch
 
+        B, H, N, D = hq.shape
+        if B != 1:
+            raise nat.NativeError("the multi-GPU layer runs batch 1")
         if self._inputs is None or self._inputs[0].shape != hq.shape:
             self._inputs = [torch.empty(hq.shape, dtype=hq.dtype, device=self.device) for _ in range(3)]
-        for src, dst in zip((hq, hk, hv), self._inputs):
-            for h in self.heads:
-                dst[:, h].copy_(src[:, h], non_blocking=True)
-        out = self(*self._inputs)
-        for h in self.heads:
-            hout[:, h].copy_(out[:, h], non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
+        if self.__dict__.get("_streams") is None:
+            self._streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+        s_in, s_out = self._streams
+        chunks, owned = self._e2e_plan(N)
+        comp = torch.cuda.current_stream(self.device)
+        b = self.step % 2
+        o = self.outs[b]
+        st = [nat.i64x4(t.stride()) for t in self._inputs]
+        with torch.cuda.device(self.device):
+            s_in.wait_stream(comp)  # the previous step's kernels are done reading the inputs
+            for hs, sub in chunks:
+                with torch.cuda.stream(s_in):
+                    for src, dst in zip((hq, hk, hv), self._inputs):
+                        for h in hs:
+                            dst[:, h].copy_(src[:, h], non_blocking=True)
+                    loaded = torch.cuda.Event()
+                    loaded.record(s_in)
+                comp.wait_event(loaded)
+                nat.check(nat.lib().svd_attn_fwd_peers(
+                    sub.handle, nat.c_void_p(self._inputs[0].data_ptr()), nat.c_void_p(self._inputs[1].data_ptr()),
+                    nat.c_void_p(self._inputs[2].data_ptr()), self.peer_ptrs[b], self.world, st[0], st[1], st[2],
+                    nat.i64x4(o.stride()), 1, int(self.head_dim), int(D), 0, nat.c_void_p(comp.cuda_stream)))
+                mine = [h for h in hs if h in owned]
+                if mine:
+                    done = torch.cuda.Event()
+                    done.record(comp)
+                    with torch.cuda.stream(s_out):
+                        s_out.wait_event(done)
+                        for h in mine:
+                            hout[:, h].copy_(o[:, h], non_blocking=True)
+            if self.world > 1:
+                nat.check(nat.lib().svd_peer_barrier(
+                    self.flag_ptrs, self.world, self.rank, nat.c_int32((self.step + 1) & 0xFFFFFFFF).value,
+                    nat.c_void_p(self.timed_out.data_ptr()), self.timeout_s, nat.c_void_p(comp.cuda_stream)))
+            rest = [h for h in self.heads if h not in owned]
+            if rest:
+                s_out.wait_stream(comp)
+                with torch.cuda.stream(s_out):
+                    for h in rest:
+                        hout[:, h].copy_(o[:, h], non_blocking=True)
+        self.step += 1
+        s_out.synchronize()
+        comp.synchronize()
         return hout
 
     def e2e_bytes(self, shape) -> tuple[int, int]:

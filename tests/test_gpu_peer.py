@@ -66,9 +66,11 @@ def _worker(rank, world, port, path, d):
         # end to end: each rank copies in its own head range, copies out that range of O
         hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
         hout = torch.full(q.shape, float("nan"), dtype=torch.bfloat16).pin_memory()
-        layer.e2e(hq, hk, hv, hout)
         hs = list(layer.heads)
-        oks.append(bool(torch.equal(hout[:, hs], ref[:, hs].cpu())))
+        for _ in range(2):  # both O buffers; chunked copy-in / shard kernels / copy-out
+            hout.fill_(float("nan"))
+            layer.e2e(hq, hk, hv, hout)
+            oks.append(bool(torch.equal(hout[:, hs], ref[:, hs].cpu())))
         sets = [None] * world
         dist.all_gather_object(sets, hs)
         oks.append(set().union(*map(set, sets)) == set(range(len(specs))))
@@ -118,6 +120,13 @@ def test_peer_path_with_split_kv(cap):
     first = layer(q, k, v).clone()
     torch.testing.assert_close(first.float(), ref.float(), atol=1.6e-2, rtol=8e-3)
     assert torch.equal(layer(q, k, v), first)
+    # the pipelined end-to-end step (head chunks through sub-shards that keep
+    # the split groups whole): the same rows, step after step
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    for _ in range(2):
+        hout = torch.full(q.shape, float("nan"), dtype=torch.bfloat16).pin_memory()
+        layer.e2e(hq, hk, hv, hout)
+        assert torch.equal(hout, first.cpu())
     assert not first[:, 2].any()
 
 
