@@ -83,3 +83,39 @@ def test_lpt_balance_hunyuan_8_ranks():
         loads = [plan.shard(world, r).info.computed_tiles for r in range(world)]
         assert sum(loads) == total
         assert max(loads) / (total / world) < 1.01
+
+
+@pytest.mark.parametrize("world,partition,cap", [(2, "heads", 0), (4, "heads", 64), (3, "items", -1)])
+def test_shard_head_subsets_partition_the_shard(world, partition, cap):
+    """svd_plan_shard_heads (a rank's pipelined end-to-end chunks): the sub-
+    shards of a partition of the rank's heads hold exactly the rank's items
+    (split-KV parts kept with their head), keep the packed row layout, and
+    reject non-shard plans / bad heads (CPU: the plan builder only)."""
+    specs = [S.full_spec(), S.diagonal_spec(1), S.skip_spec(), S.multi_diagonal_spec(),
+             S.vertical_stripe_spec(stripes=(5, 33)), S.full_spec()]
+    plan = S.LayerPlan.from_specs(specs, S.TokenLayout(96, 16, 250, 64))
+    for rank in range(world):
+        shard = plan.shard(world, rank, n_sms=148, max_item_tiles=cap, partition=partition)
+        items, _ = shard.schedule()
+        heads = shard.shard_heads()
+        parts = [heads[i::2] for i in range(2) if heads[i::2]]
+        got = []
+        for hs in parts:
+            sub = shard.shard_subset(hs)
+            sub_items, _ = sub.schedule()
+            assert set(int(h) for h in sub_items[:, 0]) <= set(hs)
+            got.append(sub_items)
+            rh, rt = sub.shard_rows()
+            sh, st = shard.shard_rows()
+            np.testing.assert_array_equal(rh, sh)
+            np.testing.assert_array_equal(rt, st)
+        merged = np.concatenate(got)
+        key = lambda a: sorted(map(tuple, a.tolist()))  # noqa: E731
+        assert key(merged) == key(items)
+    with pytest.raises(S.ConfigError):
+        plan.shard_subset((0,))  # not a shard plan
+    shard = plan.shard(2, 0)
+    with pytest.raises(S.ConfigError):
+        shard.shard_subset((0, 0))
+    with pytest.raises(S.ConfigError):
+        shard.shard_subset((len(specs),))
