@@ -129,7 +129,7 @@ class ClockSampler:
             import pynvml
 
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            h = self._nvml_handle(pynvml)
             self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
             self._nvml = (pynvml, h)
             self.thread = threading.Thread(target=self._poll, daemon=True)
@@ -147,6 +147,17 @@ class ClockSampler:
         except OSError:
             self.proc = None
         return self
+
+    def _nvml_handle(self, nv):
+        """The NVML handle of torch's device `index` (by UUID: NVML indices
+        ignore CUDA_VISIBLE_DEVICES); the NVML index as a fallback."""
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            return nv.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
 
     def _poll(self):
         nv, h = self._nvml
